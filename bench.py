@@ -1,0 +1,433 @@
+#!/usr/bin/env python
+"""Bench: cone-beam Ax / Atb GUPS on B200 (BASELINE.json metric).
+
+One *step* = one pass of the loop hot path over config 2:
+interpolated Ax over the rank's 360 angles of a 512^3 volume onto a 512^2
+detector + matched (exact-adjoint) Atb of the whole scan into the rank's
+axial slab -- the operator pair every OS-SART / SIRT / CGLS iteration
+applies (algorithms.py:213-216, :280-283).  Unit: voxel x angle updates.
+
+Multi-GPU (torchrun, one rank per GPU): weak scaling with the paper's
+splits -- the scan has 360 x N angles; rank r projects its own 360 angles
+of the full volume (angle split, scheduler.py:164-166) and backprojects all
+360 x N angles into its 512/N-slice slab (slab split).  Per-rank work is
+fixed, no collective sits in the data path.  Inputs (512 MiB volume, >= 360
+MiB stack) exceed the 126 MB L2, so no flush is needed between steps.
+
+Also reported: per-operator GUPS (Ax, matched Atb, FDK Atb), OS-SART s/iter
+(block 36, rank 0 at N=1), the roofline of the dominant kernel, the CPU
+oracle on a bounded sample, the end-to-end number through the public API
+with host buffers, SM clocks during the timed region.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_VOX = 512
+N_ANG = 360
+N_DET = 512
+METRIC = "Ax/Atb GUPS (voxel x angle updates/s), interp Ax + matched Atb"
+UNIT = "GUPS"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--size", type=int, default=N_VOX)
+    ap.add_argument("--angles", type=int, default=N_ANG)
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip OS-SART / e2e / CPU baseline (profiling runs)")
+    ap.add_argument("--cpu-sample-angles", type=int, default=4)
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def make_geometry(n, n_angles, cs):
+    """SURVEY 8(d) make_geo: dso = 2N, dsd = 4N, 1 mm voxels, pitch
+    2 sqrt(2) N / N_det, angles over 2 pi."""
+    import numpy as np
+    mag = 2.0
+    diag = math.sqrt(2.0) * n
+    det = cs.DetectorGrid(n, n, (mag * diag / n, mag * max(diag, n) / n))
+    angles = tuple(np.linspace(0.0, 2 * math.pi, n_angles, endpoint=False))
+    return cs.ScanGeometry(2.0 * n, 4.0 * n, angles, cs.VoxelGrid(n, n, n),
+                           det)
+
+
+def bytes_per_update(n, n_det):
+    """4 (1 + Nu Nv / Nvox) B per voxel-angle update."""
+    return 4.0 * (1.0 + n_det * n_det / float(n ** 3))
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 7:
+                    rows.append(f)
+        except OSError:
+            pass
+        finally:
+            if self.path:
+                os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
+                    "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        load = [r for r in rows if r[6] not in ("0", "[N/A]")] or rows
+        sm = [float(r[0]) for r in load if r[0].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in load for i in range(4)
+                          if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].isdigit()
+                else None,
+                "reasons": reasons, "samples": len(load)}
+
+
+def cpu_oracle_sample(g, x_np, n_sample, threads):
+    """Oracle (C port, all host threads) on an angle window: interpolated
+    Ax + matched Atb.  Returns (GUPS, seconds, updates)."""
+    import numpy as np
+    from oracle import oracle as O
+    og = O.OGeom(g.dso, g.dsd, g.angles, g.voxel_grid.n_x, g.voxel_grid.n_y,
+                 g.voxel_grid.n_z, nu=g.detector.n_u, nv=g.detector.n_v,
+                 pixel=g.detector.pixel_size)
+    win = (0, n_sample)
+    t0 = time.perf_counter()
+    p = O.fwd_interp(x_np, og, win, threads=threads)
+    O.bwd_matched(p, og, win, threads=threads)
+    dt = time.perf_counter() - t0
+    upd = 2.0 * n_sample * float(x_np.size)
+    del np
+    return upd / dt / 1e9, dt, upd
+
+
+def load_traffic(kernel_key):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    --set full summary (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(path))
+        return d.get(kernel_key)
+    except (OSError, ValueError):
+        return None
+
+
+def measured_peak():
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "measured"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------------
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import numpy as np
+    import paper_1905_03748_b200 as cs
+    from oracle import oracle as O
+    O.lib()
+    g = make_geometry(args.size, args.angles, cs)
+    x = cs.phantom(cs.PhantomKind.SHEPP_LOGAN_3D, g.voxel_grid).data
+    threads = O.default_threads()
+    n_s = max(1, min(args.cpu_sample_angles, args.angles))
+    for _ in range(args.warmup):
+        cpu_oracle_sample(g, x, n_s, threads)
+    times = []
+    upd = 0.0
+    for _ in range(args.steps):
+        _, dt, upd = cpu_oracle_sample(g, x, n_s, threads)
+        times.append(dt)
+    tot = sum(times)
+    val = upd * args.steps / tot / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (Shepp-Logan 3D phantom)",
+        "config": {"workload": f"config 2: {args.size}^3 volume, "
+                   f"{args.size}^2 detector, {args.angles} angles; "
+                   "interp Ax + matched Atb", "sample": f"{n_s}-angle window"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads,
+                         "kind": "port",
+                         "sample": f"{n_s}-angle window of the "
+                         f"{args.angles}-angle scan per step (outputs are "
+                         "exact slices of the full run)"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    del np
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1905_03748_b200 as cs
+    from paper_1905_03748_b200 import kernels as K
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, A1 = args.size, args.angles
+    A = A1 * world
+    g = make_geometry(n, A, cs)
+    dev = torch.device("cuda", local)
+    a0, a1 = rank * A1, (rank + 1) * A1                      # Ax: angle split
+    z0, z1 = n * rank // world, n * (rank + 1) // world      # Atb: slab split
+    nz_s = z1 - z0
+
+    vol = cs.phantom(cs.PhantomKind.SHEPP_LOGAN_3D, g.voxel_grid,
+                     device=dev).data
+    proj = torch.empty((A1, n, n), dtype=torch.float32, device=dev)
+    y = torch.empty((A, n, n), dtype=torch.float32, device=dev)
+    K.fwd_interp(vol, g, (0, A), (0, n), y)                  # Atb input
+    slab = torch.zeros((nz_s, n, n), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)]
+          for _ in range(args.steps)]
+
+    def step(e=None):
+        if e:
+            e[0].record(stream)
+        K.fwd_interp(vol, g, (a0, a1), (0, n), proj)
+        if e:
+            e[1].record(stream)
+        K.fill(slab, 0.0)
+        K.bwd_matched(y, g, (0, A), (z0, z1), slab)
+        if e:
+            e[2].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(ev[i])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    elapsed = t_start.elapsed_time(t_end) * 1e-3
+    t_ax = sum(e[0].elapsed_time(e[1]) for e in ev) * 1e-3 / args.steps
+    t_atb = sum(e[1].elapsed_time(e[2]) for e in ev) * 1e-3 / args.steps
+    if world > 1:
+        t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    upd_ax = float(A1) * n ** 3
+    upd_atb = float(A) * nz_s * n * n
+    upd_step_rank = upd_ax + upd_atb
+    total_upd = upd_step_rank * world * args.steps   # weak: equal per rank
+    value = total_upd / elapsed / 1e9
+    clocks = clk.summary()
+
+    extras = {}
+    if not args.no_extras:
+        extras = run_extras(args, cs, K, g, vol, y, dev, rank, world,
+                            (a0, a1), (z0, z1))
+
+    # dominant kernel roofline (bytes per SURVEY 8(d))
+    bpu = bytes_per_update(n, n)
+    if t_atb >= t_ax:
+        kname, kt, kupd = "bwd_matched_kernel", t_atb, upd_atb
+    else:
+        kname, kt, kupd = "fwd_interp_kernel", t_ax, upd_ax
+    peak, peak_kind = measured_peak()
+    achieved = kupd * bpu / kt / 1e9
+    traffic = load_traffic(kname)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup),
+        "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (Shepp-Logan 3D phantom; Atb input = its Ax)",
+        "config": {"workload": f"config 2 per GPU: {n}^3 volume, {n}^2 "
+                   f"detector, {A1} angles/GPU (scan of {A}); interp Ax "
+                   "(angle split) + matched Atb (slab split)",
+                   "l2": "inputs > L2 (512 MiB volume, 360+ MiB stack)",
+                   "parallelism": f"angle/slab split x{world}"},
+        "ax_gups": upd_ax / t_ax / 1e9,
+        "atb_matched_gups": upd_atb / t_atb / 1e9,
+        "roofline": {"bound": "hbm", "kernel": kname,
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": peak_kind,
+                     "bytes_per_update": bpu,
+                     "launch_ms": kt * 1e3},
+        "clocks": clocks,
+        "gpu_launches": 3 * args.steps,
+    }
+    line.update(extras)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    del np
+    return 0
+
+
+def run_extras(args, cs, K, g, vol, y, dev, rank, world, arange, zrange):
+    """FDK Atb GUPS, OS-SART s/iter, e2e through the public API, CPU
+    baseline (rank 0, N = 1)."""
+    import numpy as np
+    import torch
+    out = {}
+    n = g.voxel_grid.n_x
+    A = g.n_angles
+    z0, z1 = zrange
+    slab = torch.zeros((z1 - z0, n, n), dtype=torch.float32, device=dev)
+    # FDK-weighted Atb (slab split, all angles)
+    for _ in range(2):
+        K.bwd_fdk(y, g, (0, A), zrange, slab)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+    s.record()
+    reps = 3
+    for _ in range(reps):
+        K.bwd_fdk(y, g, (0, A), zrange, slab)
+    e.record()
+    torch.cuda.synchronize()
+    out["atb_fdk_gups"] = reps * float(A) * (z1 - z0) * n * n / (
+        s.elapsed_time(e) * 1e-3) / 1e9
+
+    # end-to-end through the public API with pinned host buffers:
+    # Ax(volume host) -> projections host; Atb(projections host) -> slab host
+    a0, a1 = arange
+    vol_h = torch.empty(vol.shape, dtype=torch.float32, pin_memory=True)
+    vol_h.copy_(vol)
+    y_h = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
+    y_h.copy_(y)
+    vol_np, y_np = vol_h.numpy(), y_h.numpy()
+    IP = cs.ProjectionMethod.INTERPOLATED
+
+    def e2e_step():
+        p = cs.forward_project_slab(cs.Volume(g.voxel_grid, vol_np), g,
+                                    (a0, a1), IP)
+        v = cs.backproject_slab(cs.ProjectionStack(g.detector, y_np), g,
+                                zrange, cs.WeightMode.MATCHED)
+        return p, v
+    e2e_step()
+    torch.cuda.synchronize()
+    ne = 3
+    t0 = time.perf_counter()
+    for _ in range(ne):
+        p, v = e2e_step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / ne
+    upd = float(a1 - a0) * n ** 3 + float(A) * (z1 - z0) * n * n
+    out["e2e"] = {"value": upd / dt / 1e9, "unit": "GUPS",
+                  "h2d_bytes_per_step": int(vol_np.nbytes + y_np.nbytes),
+                  "d2h_bytes_per_step": int(p.data.nbytes + v.data.nbytes),
+                  "ms_per_step": dt * 1e3,
+                  "api": "forward_project_slab + backproject_slab(MATCHED)"
+                         " on host numpy (pinned)"}
+    del vol_h, y_h
+
+    if world == 1:
+        # OS-SART s/iter (block 36): t(2 iters) - t(1 iter), public API
+        pool = cs.DevicePool.b200(1)
+        b = cs.ProjectionStack(g.detector, y)
+        ts = []
+        for iters in (1, 2):
+            cfg = cs.ReconConfig(pool, cs.Algorithm.OSSART, iters, 36)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            cs.os_sart(b, g, cfg)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        out["os_sart_s_per_iter"] = ts[1] - ts[0]
+        out["os_sart_setup_plus_1iter_s"] = ts[0]
+
+        from oracle import oracle as O
+        threads = O.default_threads()
+        x_np = vol.cpu().numpy()
+        n_s = max(1, min(args.cpu_sample_angles, A))
+        cpu_oracle_sample(g, x_np, 1, threads)  # warm
+        gups, dt, upd = cpu_oracle_sample(g, x_np, n_s, threads)
+        out["cpu_baseline"] = {
+            "value": gups, "unit": "GUPS", "cores": threads, "kind": "port",
+            "sample": f"interp Ax + matched Atb over a {n_s}-angle window of "
+                      f"config 2 ({dt:.1f} s; window outputs are exact "
+                      "slices of the full scan)"}
+    del np
+    return out
+
+
+if __name__ == "__main__":
+    a = parse()
+    sys.exit(run_reference(a) if a.impl == "reference" else run_ours(a))

@@ -1,0 +1,167 @@
+/*
+ * conesplit_b200.h -- C-ABI of the B200-native cone-beam hot path.
+ *
+ * Drop-in boundary B1 of SURVEY 8(b): each entry point replaces one numba
+ * kernel of the reference package `conesplit`
+ * (/root/reference/pkg/src/conesplit/_kernels.py) or one numpy stencil of
+ * its regulariser (regularization.py), with the same argument meaning.
+ *
+ * Conventions
+ *   - Array arguments marked "device" are device pointers owned by the
+ *     caller (no allocation of caller-visible memory inside the library);
+ *     "host" arrays are read synchronously before the call returns.
+ *   - Geometry arrives flattened exactly as the reference's _flat_geometry
+ *     (projectors.py:172-194): per angle 12 doubles
+ *         src[3], det00[3], ustep[3], vstep[3]
+ *     and the grid as grid6 = {gx0, gy0, gz0, vx, vy, vz}
+ *     (projectors.py:197-202, geometry.py:64-68).
+ *   - Volumes are [z][y][x] (x fastest), projections [angle][v][u]
+ *     (u fastest), both float32 (projectors.py:81-163).
+ *   - Every call is asynchronous on `stream` (a cudaStream_t; 0 = legacy
+ *     default stream) and returns 0 on success or a negative CS_ERR_* code;
+ *     cs_last_error() returns the thread's last message.
+ *   - Accumulation is fp32 on device (the reference accumulates in fp64,
+ *     _kernels.py:3-13); per-ray set-up is fp64 with the reference's exact
+ *     operation order, so sample counts and positions are the reference's.
+ */
+#ifndef CONESPLIT_B200_H
+#define CONESPLIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CS_OK 0
+#define CS_ERR_ARG -1
+#define CS_ERR_CUDA -2
+#define CS_ERR_UNSUPPORTED -3
+
+typedef void* cs_stream_t; /* cudaStream_t */
+
+/* Library identity / diagnostics. */
+const char* cs_version(void);
+const char* cs_last_error(void);
+/* Blocks the host until `stream` drains (the only synchronising call). */
+int cs_sync(cs_stream_t stream);
+
+/* ---------------------------------------------------------------- Ax ---- */
+
+/* Interpolated (trilinear, fixed-step) forward projection of the slab
+ * vol = grid slices [z_lo, z_hi) onto n_a angles.
+ * Replaces interp_forward_chunk(vol, srcs, det00, ustep, vstep, gx0, gy0,
+ * gz0, vx, vy, vz, nx, ny, nz, z_lo, z_hi, step_max, tile_u, tile_v, out)
+ * (_kernels.py:213-275); tiles are a CPU scheduling detail and are absent.
+ *   vol  device [z_hi-z_lo][ny][nx]     geom host [n_a][12]
+ *   out  device [n_a][n_v][n_u]; overwritten (accumulate=0) or added to
+ *        (accumulate=1: the partial-projection accumulate of
+ *        execution.py:224-235 fused into the kernel epilogue). */
+int cs_fwd_interp(const float* vol, int nx, int ny, int nz, int z_lo,
+                  int z_hi, const double* grid6, const double* geom, int n_a,
+                  int n_u, int n_v, double step_max, float* out,
+                  int accumulate, cs_stream_t stream);
+
+/* OS-SART residual epilogue fused into Ax (algorithms.py:294-296):
+ *   out[r] = w[r] * (b[r] - (A vol)[r])      (w may be NULL -> 1)
+ * Full volume only (z range [0, nz)). */
+int cs_fwd_interp_residual(const float* vol, int nx, int ny, int nz,
+                           const double* grid6, const double* geom, int n_a,
+                           int n_u, int n_v, double step_max, const float* b,
+                           const float* w, float* out, cs_stream_t stream);
+
+/* Siddon (exact intersection length) forward projection of a slab.
+ * Replaces siddon_forward_chunk (_kernels.py:154-191, ray :71-151). */
+int cs_fwd_siddon(const float* vol, int nx, int ny, int nz, int z_lo,
+                  int z_hi, const double* grid6, const double* geom, int n_a,
+                  int n_u, int n_v, float* out, int accumulate,
+                  cs_stream_t stream);
+
+/* --------------------------------------------------------------- Atb ---- */
+
+/* Exact adjoint of cs_fwd_interp, accumulated into the slab
+ * vol_acc = grid slices [z_lo, z_hi).
+ * Replaces matched_backward_chunk(vol64, proj, srcs, det00, ustep, vstep,
+ * gx0.., vx.., nx, ny, nz, z_lo, z_hi, step_max) (_kernels.py:278-337).
+ *   vol_acc device [z_hi-z_lo][ny][nx] (added to)   proj device [n_a][n_v][n_u] */
+int cs_bwd_matched(float* vol_acc, int nx, int ny, int nz, int z_lo,
+                   int z_hi, const double* grid6, const double* geom, int n_a,
+                   int n_u, int n_v, double step_max, const float* proj,
+                   cs_stream_t stream);
+
+/* Voxel-driven FDK-weighted backprojection, accumulated into slab
+ * vol_acc = grid slices [z_lo, z_lo + n_slab).
+ * Replaces fdk_backward_chunk(vol64, proj, coss, sins, dso, dsd, du, dv,
+ * off_u, off_v, gx0, gy0, gz0, vx, vy, vz, z_lo, tile_x, tile_y)
+ * (_kernels.py:340-398).  cs = host [n_a][2] = (cos, sin). */
+int cs_bwd_fdk(float* vol_acc, int nx, int ny, int z_lo, int n_slab,
+               const double* grid6, const double* cs, int n_a, double dso,
+               double dsd, double du, double dv, double off_u, double off_v,
+               int n_u, int n_v, const float* proj, cs_stream_t stream);
+
+/* Per-ray fp64 set-up (t0, step, n_steps), for parity tests of the ray
+ * clip of _kernels.py:194-210.  Outputs device [n_a][n_v][n_u]. */
+int cs_ray_table(int nx, int ny, int nz, const double* grid6,
+                 const double* geom, int n_a, int n_u, int n_v,
+                 double step_max, double* t0, double* step, int64_t* n,
+                 cs_stream_t stream);
+
+/* ---------------------------------------------------------------- TV ---- */
+/* All TV kernels act on a window u[nzw][ny][nx] whose first/last planes are
+ * treated as faces (the reference's _grad/_div on a window array,
+ * regularization.py:88-110, used per halo window at :241-260).  Reductions
+ * are written as fp64 to `out_sum` (device, 1 element) deterministically.
+ * Σ over planes [core_lo, core_hi) of the window only. */
+
+/* Σ g^2 over the core, g = -div(∇u / sqrt(|∇u|^2 + 1e-8))
+ * (regularization.py:127-130, :245-251 / :147). */
+int cs_tv_grad_sumsq(const float* u, int nx, int ny, int nzw, int core_lo,
+                     int core_hi, double* out_sum, cs_stream_t stream);
+
+/* u_out = u - step * g / norm with norm = *norm_dev (device fp64 scalar);
+ * skipped (u_out = u) when norm < 1e-30 (regularization.py:150, :258-260).
+ * `scale` multiplies the norm (LocalApprox extrapolation, :252-257). */
+int cs_tv_step(const float* u, float* u_out, int nx, int ny, int nzw,
+               double step, const double* norm_sumsq_dev, double scale,
+               cs_stream_t stream);
+
+/* One Chambolle dual iteration (regularization.py:174-182):
+ *   u = f + lam div p; p += (1/12/lam) ∇u; p /= max(1, |p|)
+ * p_in/p_out device [3][nzw][ny][nx] (must not alias). */
+int cs_rof_iter(const float* f, const float* p_in, float* p_out, int nx,
+                int ny, int nzw, double lam, cs_stream_t stream);
+
+/* u = f + lam div p (regularization.py:170, :280). */
+int cs_rof_finish(const float* f, const float* p, float* u, int nx, int ny,
+                  int nzw, double lam, cs_stream_t stream);
+
+/* Σ sqrt(Δz²+Δy²+Δx²) (regularization.py:119-124), fp64 into out_sum. */
+int cs_tv_norm(const float* u, int nx, int ny, int nzw, double* out_sum,
+               cs_stream_t stream);
+
+/* --------------------------------------------- loop vector algebra ---- */
+/* Building blocks of cgls / os_sart (algorithms.py:204-304). */
+
+/* out_sum = Σ a[i]*b[i] in fp64, deterministic (b may equal a). */
+int cs_dot(const float* a, const float* b, int64_t n, double* out_sum,
+           cs_stream_t stream);
+/* y += alpha * x, alpha read from device fp64 expression alpha = num/den
+ * (den < 1e-30 -> no-op); sign = +1/-1.  (CGLS x += αp, r -= αq) */
+int cs_axpy_ratio(float* y, const float* x, int64_t n, const double* num,
+                  const double* den, double sign, cs_stream_t stream);
+/* p = s + (num/den) * p  (CGLS direction update, algorithms.py:243-244) */
+int cs_xpay_ratio(float* p, const float* s, int64_t n, const double* num,
+                  const double* den, cs_stream_t stream);
+/* out = a >= 1e-8 ? 1/a : 0  (algorithms.py:254-258) */
+int cs_guarded_inverse(const float* a, float* out, int64_t n,
+                       cs_stream_t stream);
+/* x += lam * v * upd; upd = 0  (algorithms.py:298 + buffer reset) */
+int cs_sart_update(float* x, float* upd, const float* v, double lam,
+                   int64_t n, cs_stream_t stream);
+/* x = value */
+int cs_fill(float* x, float value, int64_t n, cs_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CONESPLIT_B200_H */

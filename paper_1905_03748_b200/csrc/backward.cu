@@ -1,0 +1,272 @@
+// backward.cu -- Atb on sm_100a: the exact (matched) adjoint of the
+// interpolated projector (K2) and the voxel-driven FDK backprojector (K3).
+//
+// K2 replaces the reference's single-threaded scatter
+// (_kernels.py:278-337): one thread per ray replays K1's ray set-up and
+// sample lattice bit-for-bit (shared code in common.cuh) and scatters
+// proj*step*w_corner with fp32 reductions (RED.ADD.F32) into the slab.
+// Consecutive samples that share a base voxel are merged in registers
+// before they hit L2, which halves the reduction count along the ray.
+//
+// K3 replaces fdk_backward_chunk (_kernels.py:340-398): one thread per
+// (x, y) column and FDK_ZB consecutive z voxels held in registers; the
+// column-angle terms (U, magnification, u coordinate, (dso/U)^2) are fp64
+// once per column and angle, the z walk is fp32 relative to an integer
+// detector row so the v coordinate keeps ~1e-6 px accuracy; the 2x2
+// detector footprint comes from one tld4 gather on a 2D-layered texture of
+// the projections (layers = angles) with border = 0 (the reference's
+// out-of-detector taps, :385-394).
+#include "common.cuh"
+
+namespace cs {
+
+__device__ __forceinline__ void red_add(float* p, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(128)
+    bwd_matched_kernel(float* __restrict__ vol,
+                       const AngleGeom* __restrict__ geom, Grid G,
+                       double step_max, int z_lo, int z_hi, int n_u, int n_v,
+                       const float* __restrict__ proj) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int u = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
+  const int v = blockIdx.y * 8 + (warp >> 1) * 4 + (lane >> 3);
+  const int a = blockIdx.z;
+  if (u >= n_u || v >= n_v) return;
+  const float val = __ldg(proj + ((size_t)a * n_v + v) * n_u + u);
+  if (val == 0.f) return;  // _kernels.py:295-296
+  Ray r;
+  setup_ray(geom[a], G, step_max, u, v, r);
+  if (r.n <= 0) return;
+  March m;
+  march_params(r, G, m);
+  long long k0l, k1l;
+  slab_k_range(r, m, G, z_lo, z_hi, k0l, k1l);
+  const int k0 = (int)k0l, k1 = (int)k1l, kc = (int)m.kc;
+  const int nx = G.n[0], ny = G.n[1];
+  const size_t plane = (size_t)nx * ny;
+  const float scaled = val * (float)r.step;
+
+  // Register-merged corner weights for the current base voxel.
+  int bx = INT_MIN, by = 0, bz = 0;
+  float c[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) c[i] = 0.f;
+
+  auto flush = [&]() {
+    if (bx == INT_MIN) return;
+#pragma unroll
+    for (int cz = 0; cz < 2; cz++) {
+      const int zi = bz + cz;
+      if (zi < z_lo || zi >= z_hi) continue;
+#pragma unroll
+      for (int cy = 0; cy < 2; cy++) {
+        const int yi = by + cy;
+        if (yi < 0 || yi >= ny) continue;
+#pragma unroll
+        for (int cx = 0; cx < 2; cx++) {
+          const int xi = bx + cx;
+          if (xi < 0 || xi >= nx) continue;
+          red_add(vol + (size_t)(zi - z_lo) * plane + (size_t)yi * nx + xi,
+                  c[cz * 4 + cy * 2 + cx]);
+        }
+      }
+    }
+  };
+
+  for (int k = k0; k < k1; ++k) {
+    const float kf = (float)(k - kc);
+    const float qx = fmaf(kf, m.B[0], m.A[0]);
+    const float qy = fmaf(kf, m.B[1], m.A[1]);
+    const float qz = fmaf(kf, m.B[2], m.A[2]);
+    const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
+    const float wx = qx - fx, wy = qy - fy, wz = qz - fz;
+    const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
+    if (ix != bx || iy != by || iz != bz) {
+      flush();
+      bx = ix;
+      by = iy;
+      bz = iz;
+#pragma unroll
+      for (int i = 0; i < 8; i++) c[i] = 0.f;
+    }
+    const float z0 = scaled * (1.f - wz), z1 = scaled * wz;
+    const float y00 = z0 * (1.f - wy), y01 = z0 * wy;
+    const float y10 = z1 * (1.f - wy), y11 = z1 * wy;
+    c[0] = fmaf(y00, 1.f - wx, c[0]);
+    c[1] = fmaf(y00, wx, c[1]);
+    c[2] = fmaf(y01, 1.f - wx, c[2]);
+    c[3] = fmaf(y01, wx, c[3]);
+    c[4] = fmaf(y10, 1.f - wx, c[4]);
+    c[5] = fmaf(y10, wx, c[5]);
+    c[6] = fmaf(y11, 1.f - wx, c[6]);
+    c[7] = fmaf(y11, wx, c[7]);
+  }
+  flush();
+}
+
+constexpr int FDK_ZB = 16;  // z voxels per thread (registers)
+
+__global__ void __launch_bounds__(128)
+    bwd_fdk_kernel(cudaTextureObject_t tex, const double2* __restrict__ cs,
+                   int n_a, double gx0, double gy0, double gz0, double vx,
+                   double vy, double vz, int nx, int ny, int z_lo, int n_slab,
+                   double dso, double dsd, double inv_du, double inv_dv,
+                   double off_u, double off_v, int n_u, int n_v,
+                   float* __restrict__ vol) {
+  const int ix = blockIdx.x * 32 + threadIdx.x;
+  const int iy = blockIdx.y * 4 + threadIdx.y;
+  const int zb = blockIdx.z * FDK_ZB;
+  if (ix >= nx || iy >= ny) return;
+  // voxel centres, _kernels.py:364-368
+  const double wx = gx0 + (ix + 0.5) * vx;
+  const double wy = gy0 + (iy + 0.5) * vy;
+  const double wz0 = gz0 + (z_lo + zb + 0.5) * vz;
+  const double cu = 0.5 * (n_u - 1), cv = 0.5 * (n_v - 1);
+  float acc[FDK_ZB];
+#pragma unroll
+  for (int j = 0; j < FDK_ZB; j++) acc[j] = 0.f;
+
+  for (int a = 0; a < n_a; a++) {
+    const double2 c_s = __ldg(cs + a);
+    const double c = c_s.x, s = c_s.y;
+    const double big_u = dso - (wx * c + wy * s);  // :373
+    if (big_u <= 1e-9) continue;                   // :374-375
+    const double rU = 1.0 / big_u;
+    const double mag = dsd * rU;
+    const double uf = ((-wx * s + wy * c) * mag - off_u) * inv_du + cu;
+    const double vf = (wz0 * mag - off_v) * inv_dv + cv;
+    const double wgt = dso * rU;
+    const float w2 = (float)(wgt * wgt);
+    const double fu0 = floor(uf), fv0 = floor(vf);
+    const float fu = (float)(uf - fu0);
+    const float xu = (float)fu0 + 1.f;
+    const float vfrac = (float)(vf - fv0);
+    const float vrow = (float)fv0 + 1.f;
+    const float dvz = (float)(vz * mag * inv_dv);
+#pragma unroll
+    for (int j = 0; j < FDK_ZB; j++) {
+      const float vv = fmaf((float)j, dvz, vfrac);
+      const float fl = floorf(vv);
+      const float fv = vv - fl;
+      const float4 t = gather_a2d(tex, a, xu, vrow + fl);
+      // t.w=(u0,v0) t.z=(u0+1,v0) t.x=(u0,v0+1) t.y=(u0+1,v0+1)
+      const float r0 = fmaf(fu, t.z - t.w, t.w);
+      const float r1 = fmaf(fu, t.y - t.x, t.x);
+      acc[j] = fmaf(w2, fmaf(fv, r1 - r0, r0), acc[j]);
+    }
+  }
+  const size_t plane = (size_t)nx * ny;
+  float* col = vol + (size_t)iy * nx + ix;
+#pragma unroll
+  for (int j = 0; j < FDK_ZB; j++)
+    if (zb + j < n_slab) col[(size_t)(zb + j) * plane] += acc[j];
+}
+
+__global__ void ray_table_kernel(const AngleGeom* __restrict__ geom, Grid G,
+                                 double step_max, int n_u, int n_v,
+                                 double* t0, double* step, int64_t* n) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  const int a = blockIdx.z;
+  if (u >= n_u) return;
+  Ray r;
+  setup_ray(geom[a], G, step_max, u, v, r);
+  const size_t i = ((size_t)a * n_v + v) * n_u + u;
+  t0[i] = r.t0;
+  step[i] = r.step;
+  n[i] = r.n;
+}
+
+}  // namespace cs
+
+using namespace cs;
+
+extern "C" {
+
+int cs_bwd_matched(float* vol_acc, int nx, int ny, int nz, int z_lo,
+                   int z_hi, const double* grid6, const double* geom, int n_a,
+                   int n_u, int n_v, double step_max, const float* proj,
+                   cs_stream_t stream) {
+  CS_REQUIRE(nx > 0 && ny > 0 && nz > 0, CS_ERR_ARG, "bad grid");
+  CS_REQUIRE(0 <= z_lo && z_lo < z_hi && z_hi <= nz, CS_ERR_ARG,
+             "invalid slab range [%d, %d) for nz=%d", z_lo, z_hi, nz);
+  CS_REQUIRE(n_a > 0 && n_a <= 65535 && n_u > 0 && n_v > 0, CS_ERR_ARG,
+             "bad projection shape");
+  CS_REQUIRE(step_max > 0.0, CS_ERR_ARG, "step_max must be positive");
+  cudaStream_t s = (cudaStream_t)stream;
+  const Grid G = make_grid(grid6, nx, ny, nz);
+  AngleGeom* dgeom = nullptr;
+  int rc = upload_geometry(geom, n_a, s, &dgeom);
+  if (rc) return rc;
+  const dim3 grid((n_u + 15) / 16, (n_v + 7) / 8, n_a);
+  bwd_matched_kernel<<<grid, 128, 0, s>>>(vol_acc, dgeom, G, step_max, z_lo,
+                                          z_hi, n_u, n_v, proj);
+  cudaError_t e = cudaGetLastError();
+  release_geometry(dgeom, s);
+  CS_CHECK_CUDA(e);
+  return CS_OK;
+}
+
+int cs_bwd_fdk(float* vol_acc, int nx, int ny, int z_lo, int n_slab,
+               const double* grid6, const double* cs_host, int n_a,
+               double dso, double dsd, double du, double dv, double off_u,
+               double off_v, int n_u, int n_v, const float* proj,
+               cs_stream_t stream) {
+  CS_REQUIRE(nx > 0 && ny > 0 && n_slab > 0 && z_lo >= 0, CS_ERR_ARG,
+             "bad slab");
+  CS_REQUIRE(n_a > 0 && n_u > 0 && n_v > 0, CS_ERR_ARG,
+             "bad projection shape");
+  CS_REQUIRE(du > 0 && dv > 0, CS_ERR_ARG, "pixel sizes must be positive");
+  cudaStream_t s = (cudaStream_t)stream;
+  double2* dcs = nullptr;
+  CS_CHECK_CUDA(cudaMallocAsync((void**)&dcs, sizeof(double2) * n_a, s));
+  CS_CHECK_CUDA(cudaMemcpyAsync(dcs, cs_host, sizeof(double2) * n_a,
+                                cudaMemcpyHostToDevice, s));
+  const dim3 block(32, 4);
+  const dim3 grid((nx + 31) / 32, (ny + 3) / 4,
+                  (n_slab + FDK_ZB - 1) / FDK_ZB);
+  const int maxl = max_layers();
+  const size_t sheet = (size_t)n_u * n_v;
+  int rc = CS_OK;
+  for (int a0 = 0; a0 < n_a && rc == CS_OK; a0 += maxl) {
+    const int na = min(maxl, n_a - a0);
+    LayeredTexture* t = nullptr;
+    rc = load_layered(TEX_PROJ, proj + (size_t)a0 * sheet, n_u, n_v, na, s,
+                      &t);
+    if (rc) break;
+    bwd_fdk_kernel<<<grid, block, 0, s>>>(
+        t->tex, dcs + a0, na, grid6[0], grid6[1], grid6[2], grid6[3],
+        grid6[4], grid6[5], nx, ny, z_lo, n_slab, dso, dsd, 1.0 / du,
+        1.0 / dv, off_u, off_v, n_u, n_v, vol_acc);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      set_error("bwd_fdk launch: %s", cudaGetErrorString(e));
+      rc = CS_ERR_CUDA;
+    }
+  }
+  cudaFreeAsync(dcs, s);
+  return rc;
+}
+
+int cs_ray_table(int nx, int ny, int nz, const double* grid6,
+                 const double* geom, int n_a, int n_u, int n_v,
+                 double step_max, double* t0, double* step, int64_t* n,
+                 cs_stream_t stream) {
+  CS_REQUIRE(n_a > 0 && n_a <= 65535 && n_v <= 65535, CS_ERR_ARG,
+             "bad shape");
+  cudaStream_t s = (cudaStream_t)stream;
+  const Grid G = make_grid(grid6, nx, ny, nz);
+  AngleGeom* dgeom = nullptr;
+  int rc = upload_geometry(geom, n_a, s, &dgeom);
+  if (rc) return rc;
+  ray_table_kernel<<<dim3((n_u + 127) / 128, n_v, n_a), 128, 0, s>>>(
+      dgeom, G, step_max, n_u, n_v, t0, step, n);
+  cudaError_t e = cudaGetLastError();
+  release_geometry(dgeom, s);
+  CS_CHECK_CUDA(e);
+  return CS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,247 @@
+// common.cuh -- shared device/host helpers for the conesplit B200 library.
+//
+// Error model of the C-ABI (include/conesplit_b200.h): every entry point
+// returns 0 on success or a negative code, and records a message readable
+// through cs_last_error() (thread-local).  Entry points never synchronise
+// the host; all work is enqueued on the caller's stream.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <cstdio>
+#include <string>
+
+#include "../../include/conesplit_b200.h"
+
+namespace cs {
+
+void set_error(const char* fmt, ...);
+
+#define CS_CHECK_CUDA(expr)                                                  \
+  do {                                                                       \
+    cudaError_t _e = (expr);                                                 \
+    if (_e != cudaSuccess) {                                                 \
+      ::cs::set_error("%s:%d %s -> %s", __FILE__, __LINE__, #expr,           \
+                      cudaGetErrorString(_e));                               \
+      return CS_ERR_CUDA;                                                    \
+    }                                                                        \
+  } while (0)
+
+#define CS_REQUIRE(cond, code, ...)                                          \
+  do {                                                                       \
+    if (!(cond)) {                                                           \
+      ::cs::set_error(__VA_ARGS__);                                          \
+      return (code);                                                         \
+    }                                                                        \
+  } while (0)
+
+// Voxel grid: lower corner, voxel size and counts (projectors.py:197-202).
+struct Grid {
+  double g0[3];
+  double vox[3];
+  int n[3];  // nx, ny, nz (FULL grid: ray sampling always uses the full box)
+};
+
+// Per-angle flattened geometry, projectors.py:172-194:
+//   src[3], det00[3], ustep[3], vstep[3]
+struct AngleGeom {
+  double src[3], det00[3], ustep[3], vstep[3];
+};
+
+// ---------------------------------------------------------------------------
+// fp64 ray set-up, IEEE round-to-nearest with NO contraction so that the
+// sample count n = ceil(L / step_max) and t0 / step are the reference's bits
+// (_kernels.py:28-68, :194-210, :234-246).  SURVEY 0.3: fp32 set-up flips
+// n_steps on ~1e-4 of rays at 512^3.
+
+__device__ __forceinline__ double dsub(double a, double b) {
+  return __dadd_rn(a, -b);
+}
+
+struct Ray {
+  double o[3];    // source
+  double d[3];    // unit direction
+  double t0;      // entry parameter on the full grid box
+  double step;    // L / n
+  long long n;    // number of samples (0 = miss / graze)
+};
+
+// Unit direction through pixel (u, v): _kernels.py:234-243.
+__device__ __forceinline__ void pixel_direction(const AngleGeom& g, int u,
+                                                int v, double d[3]) {
+  double t[3];
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+    t[i] = __dadd_rn(__dadd_rn(g.det00[i], __dmul_rn((double)u, g.ustep[i])),
+                     __dmul_rn((double)v, g.vstep[i]));
+  double x = dsub(t[0], g.src[0]), y = dsub(t[1], g.src[1]),
+         z = dsub(t[2], g.src[2]);
+  double ss = __dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)),
+                        __dmul_rn(z, z));
+  double inv = __ddiv_rn(1.0, __dsqrt_rn(ss));
+  d[0] = __dmul_rn(x, inv);
+  d[1] = __dmul_rn(y, inv);
+  d[2] = __dmul_rn(z, inv);
+}
+
+// Slab-method clip against [b0, b1] per axis: _kernels.py:28-68.
+// Returns false on a miss.
+__device__ __forceinline__ bool clip_box(const double o[3], const double d[3],
+                                         const double b0[3],
+                                         const double b1[3], double& t0o,
+                                         double& t1o) {
+  double t0 = -1e300, t1 = 1e300;
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    if (d[i] != 0.0) {
+      double ta = __ddiv_rn(dsub(b0[i], o[i]), d[i]);
+      double tb = __ddiv_rn(dsub(b1[i], o[i]), d[i]);
+      if (ta > tb) {
+        double tmp = ta;
+        ta = tb;
+        tb = tmp;
+      }
+      if (ta > t0) t0 = ta;
+      if (tb < t1) t1 = tb;
+    } else if (o[i] < b0[i] || o[i] > b1[i]) {
+      return false;
+    }
+  }
+  if (t0 > t1) return false;
+  t0o = t0;
+  t1o = t1;
+  return true;
+}
+
+// _kernels.py:194-210 (+ the direction of :234-243).
+__device__ __forceinline__ void setup_ray(const AngleGeom& g, const Grid& G,
+                                          double step_max, int u, int v,
+                                          Ray& r) {
+  r.o[0] = g.src[0];
+  r.o[1] = g.src[1];
+  r.o[2] = g.src[2];
+  pixel_direction(g, u, v, r.d);
+  double b0[3], b1[3];
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    b0[i] = G.g0[i];
+    b1[i] = __dadd_rn(G.g0[i], __dmul_rn((double)G.n[i], G.vox[i]));
+  }
+  double t0, t1;
+  r.n = 0;
+  r.t0 = 0.0;
+  r.step = 0.0;
+  if (!clip_box(r.o, r.d, b0, b1, t0, t1)) return;
+  double length = dsub(t1, t0);
+  if (length <= 1e-12) return;  // _EPS_LEN graze
+  double nf = ceil(__ddiv_rn(length, step_max));
+  r.n = (long long)nf;
+  r.t0 = t0;
+  r.step = __ddiv_rn(length, nf);
+}
+
+// fp32 march parameters: q(k) = A + (k - kc) * B per axis, where
+// q = (o + t d - g0) / vox - 0.5 and t = t0 + (k + 0.5) step
+// (_kernels.py:249-252).  A is evaluated in fp64 at the ray's middle
+// sample kc so the fp32 error stays ~ulp(N/2).
+struct March {
+  float A[3], B[3];
+  long long kc;
+};
+
+__device__ __forceinline__ void march_params(const Ray& r, const Grid& G,
+                                             March& m) {
+  m.kc = r.n >> 1;
+  double tc = r.t0 + ((double)m.kc + 0.5) * r.step;
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    m.A[i] = (float)((r.o[i] + tc * r.d[i] - G.g0[i]) / G.vox[i] - 0.5);
+    m.B[i] = (float)(r.step * r.d[i] / G.vox[i]);
+  }
+}
+
+// Sample range [k0, k1) whose trilinear z-support can touch global slices
+// [z_lo, z_hi): qz(k) in [z_lo - 1, z_hi).  Conservative by two samples;
+// exact slab membership is decided per tap in the march loop with the same
+// fp32 qz a monolithic launch computes, so slab partial sums add up to the
+// monolithic result.
+__device__ __forceinline__ void slab_k_range(const Ray& r, const March& m,
+                                             const Grid& G, int z_lo,
+                                             int z_hi, long long& k0,
+                                             long long& k1) {
+  k0 = 0;
+  k1 = r.n;
+  if (z_lo <= 0 && z_hi >= G.n[2]) return;
+  double B = (double)m.B[2], A = (double)m.A[2];
+  double lo = (double)z_lo - 1.0, hi = (double)z_hi;
+  if (fabs(B) < 1e-30) {
+    if (A < lo - 1.0 || A > hi + 1.0) k1 = 0;
+    return;
+  }
+  double ka = (lo - A) / B + (double)m.kc, kb = (hi - A) / B + (double)m.kc;
+  if (ka > kb) {
+    double t = ka;
+    ka = kb;
+    kb = t;
+  }
+  double fa = floor(ka) - 2.0, fb = ceil(kb) + 3.0;
+  if (fa > 0.0) k0 = fa > (double)r.n ? r.n : (long long)fa;
+  if (fb < (double)r.n) k1 = fb < 0.0 ? 0 : (long long)fb;
+}
+
+// tld4 (gather) on a 2D layered float texture: returns the 2x2 footprint a
+// bilinear fetch at (x, y) would use.  With x = i + 1, y = j + 1 (unnormalised
+// coordinates) the footprint is texels i..i+1 x j..j+1.  Component order
+// (PTX tld4): x = (i, j+1), y = (i+1, j+1), z = (i+1, j), w = (i, j).
+// Border address mode supplies the reference's zero padding in x and y
+// (_kernels.py:264-272; FDK :385-394); layers are clamped by hardware, so
+// callers mask layers themselves.
+__device__ __forceinline__ float4 gather_a2d(cudaTextureObject_t t, int layer,
+                                             float x, float y) {
+  float4 r;
+  asm volatile(
+      "tld4.r.a2d.v4.f32.f32 {%0, %1, %2, %3}, [%4, {%5, %6, %7, %8}];"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "l"(t), "r"(layer), "f"(x), "f"(y), "f"(0.f));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Host side: per-(device, stream) layered-texture cache.  A volume slab
+// [n_slab, ny, nx] becomes a cudaArray with nx x ny layers; a projection
+// stack [n_a, n_v, n_u] becomes n_u x n_v layers.
+struct LayeredTexture {
+  cudaArray_t array = nullptr;
+  cudaTextureObject_t tex = 0;
+  int w = 0, h = 0, layers = 0;
+};
+
+enum TexRole { TEX_VOLUME = 0, TEX_PROJ = 1 };
+
+// Returns a texture whose array is (w, h, >= layers) and loads `layers`
+// layers from the linear array `src` ([layers][h][w], device or host
+// memory) on stream s.
+int load_layered(TexRole role, const float* src, int w, int h, int layers,
+                 cudaStream_t s, LayeredTexture** out);
+
+// Max layers of a 2D layered texture on this device (2048 on sm_100).
+int max_layers();
+
+// Geometry tables copied to the device (stream-ordered allocation).
+int upload_geometry(const double* geom, int n_a, cudaStream_t s,
+                    AngleGeom** d_geom);
+void release_geometry(AngleGeom* d_geom, cudaStream_t s);
+
+Grid make_grid(const double grid6[6], int nx, int ny, int nz);
+
+inline int num_sms() {
+  static int sms = -1;
+  if (sms < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+}  // namespace cs

@@ -1,0 +1,319 @@
+"""CUDA path vs the oracle / reference goldens (the parity gate).
+
+Tolerances (SURVEY 8(c), fp32 device accumulation vs fp64 reference):
+  Ax interpolated  relL2 <= 1e-5, max-rel <= 1e-4
+  Atb matched      relL2 <= 1e-5; adjoint identity <= 1e-5
+  Atb FDK          relL2 <= 1e-5
+  Siddon Ax        relL2 <= 1e-5
+  TV step         relL2 <= 1e-5
+  loops            relL2 <= 3e-5 (3x the operator tolerance)
+  integer set-up   bit-exact (ray t0/step/n_steps, slab/angle ranges)
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_1905_03748_b200 as cs
+from paper_1905_03748_b200 import kernels as K
+from conftest import (max_rel, product_geometry, rel_l2, synth_geometry,
+                      to_oracle)
+from oracle import oracle as O
+
+GEOS = ["g16", "ganiso", "g32"]
+IP = cs.ProjectionMethod.INTERPOLATED
+SD = cs.ProjectionMethod.SIDDON
+TOL_OP = 1e-5
+TOL_LOOP = 3e-5
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+
+
+@pytest.mark.parametrize("name", GEOS)
+def test_ray_setup_bit_exact(golden, golden_meta, name):
+    g = product_geometry(golden_meta["geometries"][name])
+    t0, st, n = K.ray_table(g, (0, g.n_angles))
+    np.testing.assert_array_equal(t0.cpu().numpy(), golden[f"{name}/ray_t0"])
+    np.testing.assert_array_equal(st.cpu().numpy(), golden[f"{name}/ray_step"])
+    np.testing.assert_array_equal(n.cpu().numpy(), golden[f"{name}/ray_n"])
+
+
+@pytest.mark.parametrize("name", GEOS)
+def test_forward_vs_reference(golden, golden_meta, name):
+    d = golden_meta["geometries"][name]
+    g = product_geometry(d)
+    x = golden[f"{name}/x"]
+    vol = cs.Volume(g.voxel_grid, x)
+    A = g.n_angles
+    got = cs.forward_project_slab(vol, g, (0, A), IP).data
+    ref = golden[f"{name}/fwd_interp"]
+    assert rel_l2(got, ref) <= TOL_OP and max_rel(got, ref) <= 1e-4
+    got = cs.forward_project_slab(vol, g, (0, A), SD).data
+    assert rel_l2(got, golden[f"{name}/fwd_siddon"]) <= TOL_OP
+    z0, z1 = d["slab"]
+    a0, a1 = d["window"]
+    slab = cs.Volume(g.voxel_grid, x[z0:z1], (z0, z1))
+    got = cs.forward_project_slab(slab, g, (a0, a1), IP).data
+    assert rel_l2(got, golden[f"{name}/fwd_interp_slab"]) <= TOL_OP
+    got = cs.forward_project_slab(slab, g, (a0, a1), SD).data
+    assert rel_l2(got, golden[f"{name}/fwd_siddon_slab"]) <= TOL_OP
+
+
+@pytest.mark.parametrize("name", GEOS)
+def test_backward_vs_reference(golden, golden_meta, name):
+    d = golden_meta["geometries"][name]
+    g = product_geometry(d)
+    x, y = golden[f"{name}/x"], golden[f"{name}/y"]
+    A, nz = g.n_angles, g.voxel_grid.n_z
+    stack = cs.ProjectionStack(g.detector, y, (0, A))
+    for mode, key in ((cs.WeightMode.MATCHED, "bwd_matched"),
+                      (cs.WeightMode.FDK, "bwd_fdk")):
+        got = cs.backproject_slab(stack, g, (0, nz), mode).data
+        assert rel_l2(got, golden[f"{name}/{key}"]) <= TOL_OP, key
+        z0, z1 = d["slab"]
+        a0, a1 = d["window"]
+        sub = cs.ProjectionStack(g.detector, y[a0:a1], (a0, a1))
+        acc = cs.Volume(g.voxel_grid, x[z0:z1] * 0.5, (z0, z1))
+        got = cs.backproject_slab(sub, g, (z0, z1), mode,
+                                  accumulate_into=acc).data
+        assert rel_l2(got, golden[f"{name}/{key}_slab"]) <= TOL_OP, key
+
+
+def test_kat_cube(golden, golden_meta):
+    g = product_geometry(golden_meta["kat_cube"])
+    vol = cs.Volume(g.voxel_grid, np.full((10, 10, 10), 0.02, np.float32))
+    s = cs.forward_project_slab(vol, g, (0, 1), SD).data
+    assert abs(s[0, 1, 1] - 0.2) < 1e-4
+    i = cs.forward_project_slab(vol, g, (0, 1), IP).data
+    np.testing.assert_allclose(i, golden["kat/cube_interp"], rtol=1e-5,
+                               atol=1e-7)
+
+
+@pytest.mark.parametrize("n,na", [(16, 8), (40, 13)])
+def test_adjoint_identity(n, na):
+    """<A x, y> == <x, A^T y>."""
+    g = synth_geometry(n, na, nu=n + 8, nv=n + 4)
+    rng = np.random.default_rng(3)
+    for _ in range(5):
+        x = dev(rng.random((n, n, n)))
+        y = dev(rng.standard_normal((na, n + 4, n + 8)))
+        ax = torch.empty_like(y)
+        K.fwd_interp(x, g, (0, na), (0, n), ax)
+        aty = torch.zeros_like(x)
+        K.bwd_matched(y, g, (0, na), (0, n), aty)
+        lhs = float((ax.double() * y.double()).sum())
+        rhs = float((x.double() * aty.double()).sum())
+        assert abs(lhs - rhs) <= TOL_OP * max(abs(lhs), abs(rhs))
+
+
+def test_dense_matrix_adjoint_8():
+    """dense 8^3 matrix from unit basis vectors; A^T == A.T."""
+    g = synth_geometry(8, 3, nu=10, nv=9)
+    nvox = 8 ** 3
+    cols = []
+    basis = torch.zeros(nvox, device="cuda")
+    out = torch.empty((3, 9, 10), device="cuda")
+    for j in range(nvox):
+        basis.zero_()
+        basis[j] = 1.0
+        K.fwd_interp(basis.view(8, 8, 8), g, (0, 3), (0, 8), out)
+        cols.append(out.flatten().cpu().numpy().copy())
+    Amat = np.stack(cols, 1).astype(np.float64)
+    rows = []
+    e = torch.zeros(3 * 9 * 10, device="cuda")
+    acc = torch.zeros((8, 8, 8), device="cuda")
+    for i in range(0, 3 * 9 * 10):
+        e.zero_()
+        e[i] = 1.0
+        acc.zero_()
+        K.bwd_matched(e.view(3, 9, 10), g, (0, 3), (0, 8), acc)
+        rows.append(acc.flatten().cpu().numpy().copy())
+    ATmat = np.stack(rows, 0).astype(np.float64)
+    assert np.abs(Amat - ATmat).max() <= 1e-6 * np.abs(Amat).max()
+
+
+def test_c1_operators_vs_oracle():
+    """Config 1 (64^3, 64^2, 100 angles): full operators vs the oracle."""
+    g = synth_geometry(64, 100)
+    og = to_oracle(g)
+    x = np.random.default_rng(0).random((64, 64, 64), dtype=np.float32)
+    y = np.random.default_rng(1).standard_normal((100, 64, 64)).astype(
+        np.float32)
+    ax = torch.empty((100, 64, 64), device="cuda")
+    K.fwd_interp(dev(x), g, (0, 100), (0, 64), ax)
+    ref = O.fwd_interp(x, og)
+    assert rel_l2(ax.cpu(), ref) <= TOL_OP
+    assert max_rel(ax.cpu(), ref) <= 1e-4
+    for fn, ofn in ((K.bwd_matched, O.bwd_matched), (K.bwd_fdk, O.bwd_fdk)):
+        acc = torch.zeros((64, 64, 64), device="cuda")
+        fn(dev(y), g, (0, 100), (0, 64), acc)
+        assert rel_l2(acc.cpu(), ofn(y, og)) <= TOL_OP, fn.__name__
+
+
+def test_slab_partition_transparency():
+    """Forward slab partials sum to the monolithic projection; backward
+    slabs concatenate to the monolithic volume."""
+    n, na = 48, 36
+    g = synth_geometry(n, na)
+    x = dev(np.random.default_rng(0).random((n, n, n)))
+    y = dev(np.random.default_rng(1).standard_normal((na, n, n)))
+    mono = torch.empty((na, n, n), device="cuda")
+    K.fwd_interp(x, g, (0, na), (0, n), mono)
+    for cuts in [(0, 20, 41, 48), (0, 1, 2, 47, 48), (0, 16, 32, 48)]:
+        acc = torch.empty_like(mono)
+        for i, (z0, z1) in enumerate(zip(cuts[:-1], cuts[1:])):
+            K.fwd_interp(x[z0:z1].contiguous(), g, (0, na), (z0, z1), acc,
+                         accumulate=i > 0)
+        assert rel_l2(acc.cpu(), mono.cpu()) <= 1e-6
+    for fn in (K.bwd_matched, K.bwd_fdk):
+        whole = torch.zeros((n, n, n), device="cuda")
+        fn(y, g, (0, na), (0, n), whole)
+        parts = torch.zeros_like(whole)
+        for z0, z1 in [(0, 20), (20, 41), (41, 48)]:
+            fn(y, g, (0, na), (z0, z1), parts[z0:z1])
+        assert rel_l2(parts.cpu(), whole.cpu()) <= 1e-6
+
+
+def test_angle_window_invariance():
+    g = synth_geometry(32, 20)
+    x = dev(np.random.default_rng(0).random((32, 32, 32)))
+    full = torch.empty((20, 32, 32), device="cuda")
+    K.fwd_interp(x, g, (0, 20), (0, 32), full)
+    win = torch.empty((10, 32, 32), device="cuda")
+    K.fwd_interp(x, g, (10, 20), (0, 32), win)
+    assert torch.equal(win, full[10:20])
+
+
+def test_edge_cases():
+    """Rays missing the grid, single angle, zero projections."""
+    grid = cs.VoxelGrid(8, 8, 8)
+    det = cs.DetectorGrid(40, 30, (2.0, 2.0))  # panel much wider than shadow
+    g = cs.ScanGeometry(40.0, 80.0, (0.3,), grid, det)
+    og = to_oracle(g)
+    x = np.random.default_rng(5).random((8, 8, 8), dtype=np.float32)
+    got = cs.forward_project_slab(cs.Volume(grid, x), g, (0, 1), IP).data
+    ref = O.fwd_interp(x, og)
+    assert (ref == 0).sum() > 100  # many misses
+    assert np.array_equal(got == 0, ref == 0)
+    assert rel_l2(got, ref) <= TOL_OP
+    zero = cs.ProjectionStack(det, np.zeros((1, 30, 40), np.float32))
+    for mode in cs.WeightMode:
+        out = cs.backproject_slab(zero, g, (0, 8), mode).data
+        assert not out.any()
+
+
+def test_tv_vs_reference(golden):
+    f = golden["tv/f"]
+    grid = cs.VoxelGrid(20, 18, 24)
+    vol = cs.Volume(grid, f)
+    assert abs(cs.tv_norm(vol) - float(golden["tv/norm"])) <= \
+        1e-6 * float(golden["tv/norm"])
+    single = np.zeros((3, 3, 3), np.float32)
+    single[1, 1, 1] = 1.0
+    assert abs(cs.tv_norm(cs.Volume(cs.VoxelGrid(3, 3, 3), single))
+               - (math.sqrt(3) + 3)) < 1e-6
+    GD, ROF = cs.TvMinimizer.GRADIENT_DESCENT, cs.TvMinimizer.ROF
+    got = cs.minimize_tv_gradient(vol, cs.TvParams(GD, inner_iters=12,
+                                                   step=0.05)).data
+    assert rel_l2(got, golden["tv/gd"]) <= TOL_OP
+    got = cs.minimize_rof(vol, cs.TvParams(ROF, inner_iters=12, lam=0.1)).data
+    assert rel_l2(got, golden["tv/rof"]) <= TOL_OP
+    for ndev in (1, 2, 3):
+        pool = cs.DevicePool(tuple(cs.DeviceSpec(memory_budget=10 ** 9)
+                                   for _ in range(ndev)))
+        for minim, tag in ((GD, "gd"), (ROF, "rof")):
+            for nm, ntag in ((cs.NormMode.EXACT_GLOBAL, "exact"),
+                             (cs.NormMode.LOCAL_APPROX, "local")):
+                if minim is ROF and ntag == "local":
+                    continue
+                p = cs.TvParams(minim, outer_syncs=2, inner_iters=4,
+                                step=0.05, lam=0.1, norm_mode=nm,
+                                halo_depth=5)
+                got = cs.split_minimize(vol, pool, p).data
+                key = f"tv/split_{tag}_{ntag}_d{ndev}"
+                assert rel_l2(got, golden[key]) <= TOL_OP, key
+
+
+def test_loops_vs_reference(golden, golden_meta):
+    g = product_geometry(golden_meta["geometries"]["g16"])
+    pool = cs.DevicePool((cs.DeviceSpec(memory_budget=2 ** 30),))
+    b = cs.ProjectionStack(g.detector, golden["loops/b16"])
+    res = cs.cgls(b, g, cs.ReconConfig(pool, iterations=4))
+    assert rel_l2(res.volume.data, golden["loops/cgls_x"]) <= TOL_LOOP
+    np.testing.assert_allclose(res.residuals, golden["loops/cgls_res"],
+                               rtol=TOL_LOOP)
+    got = cs.os_sart(b, g, cs.ReconConfig(pool, cs.Algorithm.OSSART, 3,
+                                          g.n_angles)).data
+    assert rel_l2(got, golden["loops/sirt_x"]) <= TOL_LOOP
+    got = cs.os_sart(b, g, cs.ReconConfig(pool, cs.Algorithm.OSSART, 2, 3,
+                                          0.8)).data
+    assert rel_l2(got, golden["loops/ossart_x"]) <= TOL_LOOP
+    tv = cs.TvParams(cs.TvMinimizer.GRADIENT_DESCENT, inner_iters=5,
+                     step=0.01)
+    got = cs.os_sart(b, g, cs.ReconConfig(pool, cs.Algorithm.OSSART, 2, 4,
+                                          tv=tv)).data
+    assert rel_l2(got, golden["loops/sarttv_x"]) <= TOL_LOOP
+    got = cs.fdk(b, g, pool).data
+    assert rel_l2(got, golden["loops/fdk_x"]) <= TOL_LOOP
+
+
+def test_executor_split_transparency():
+    """execute_forward / execute_backward == monolithic for {1,2,3}
+    devices x forced splits, and traces respect budgets."""
+    n, na = 24, 12
+    g = synth_geometry(n, na)
+    x = np.random.default_rng(0).random((n, n, n), dtype=np.float32)
+    y = np.random.default_rng(1).standard_normal((na, n, n)).astype(
+        np.float32)
+    vol = cs.Volume(g.voxel_grid, x)
+    stack = cs.ProjectionStack(g.detector, y)
+    mono_f = cs.forward_project_slab(vol, g, (0, na), IP).data
+    mono_b = cs.backproject_slab(stack, g, (0, n), cs.WeightMode.MATCHED).data
+    plane = n * n * 4
+    chunk = 9 * n * n * 4
+    for ndev in (1, 2, 3):
+        for budget in (10 ** 9, (n // 2) * plane + 4 * chunk,
+                       (n // 3) * plane + 4 * chunk):
+            pool = cs.DevicePool(tuple(cs.DeviceSpec(memory_budget=budget)
+                                       for _ in range(ndev)))
+            fplan = cs.plan_forward(g, pool)
+            bplan = cs.plan_backward(g, pool)
+            sink = []
+            f = cs.execute_forward(vol, g, pool, fplan, IP, trace_sink=sink)
+            assert rel_l2(f.data, mono_f) <= 1e-6
+            b = cs.execute_backward(stack, g, pool, bplan,
+                                    cs.WeightMode.MATCHED, trace_sink=sink)
+            assert rel_l2(b.data, mono_b) <= 1e-6
+            assert len(sink) == 2 and all(not t.simulated for t in sink)
+            assert any(e.kind == "Kernel" for e in sink[0].events)
+
+
+def test_device_resident_roundtrip():
+    """Device tensors in -> device tensors out, no host staging."""
+    g = synth_geometry(32, 10)
+    x = torch.rand((32, 32, 32), device="cuda")
+    p = cs.forward_project_slab(cs.Volume(g.voxel_grid, x), g, (0, 10), IP)
+    assert isinstance(p.data, torch.Tensor) and p.data.is_cuda
+    v = cs.backproject_slab(p, g, (0, 32), cs.WeightMode.MATCHED)
+    assert isinstance(v.data, torch.Tensor) and v.data.is_cuda
+    ref = O.bwd_matched(p.data.cpu().numpy(), to_oracle(g))
+    assert rel_l2(v.data.cpu(), ref) <= TOL_OP
+
+
+def test_tigre_aliases():
+    g = synth_geometry(16, 6)
+    x = np.random.default_rng(0).random((16, 16, 16), dtype=np.float32)
+    p = cs.Ax(x, g)
+    assert rel_l2(p, O.fwd_interp(x, to_oracle(g))) <= TOL_OP
+    v = cs.Atb(p, g, weight="fdk")
+    assert rel_l2(v, O.bwd_fdk(p, to_oracle(g))) <= TOL_OP
+    r = cs.sirt(p, g, niter=2)
+    assert r.shape == (16, 16, 16)
