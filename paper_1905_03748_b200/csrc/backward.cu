@@ -16,6 +16,8 @@
 // detector footprint comes from one tld4 gather on a 2D-layered texture of
 // the projections (layers = angles) with border = 0 (the reference's
 // out-of-detector taps, :385-394).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cs {
@@ -24,6 +26,37 @@ __device__ __forceinline__ void red_add(float* p, float v) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+// One 16-byte vector reduction (REDG.E.ADD.F32x4) on an aligned group.
+__device__ __forceinline__ void red_add4(float* p, float a, float b, float c,
+                                         float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p),
+               "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+// Adds (c0, c1) at x = bx, bx + 1 of one row (row 16-byte aligned, nx % 4
+// == 0).  Both taps usually sit in one aligned float4 group -> one vector
+// reduction (zeros elsewhere); otherwise per-tap scalar reductions.
+__device__ __forceinline__ void red_pair(float* row, int bx, int nx, float c0,
+                                         float c1) {
+  const int lane = bx & 3;
+  if (bx >= 0 && lane <= 2 && bx + 1 < nx) {
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      if (i == lane) {
+        v[i] = c0;
+        v[i + 1] = c1;
+      }
+    }
+    red_add4(row + (bx - lane), v[0], v[1], v[2], v[3]);
+    return;
+  }
+  if (bx >= 0 && bx < nx) red_add(row + bx, c0);
+  if (bx + 1 >= 0 && bx + 1 < nx) red_add(row + bx + 1, c1);
+}
+
+template <bool V4>
 __global__ void __launch_bounds__(128)
     bwd_matched_kernel(float* __restrict__ vol,
                        const AngleGeom* __restrict__ geom, Grid G,
@@ -64,6 +97,11 @@ __global__ void __launch_bounds__(128)
       for (int cy = 0; cy < 2; cy++) {
         const int yi = by + cy;
         if (yi < 0 || yi >= ny) continue;
+        if (V4) {
+          red_pair(vol + (size_t)(zi - z_lo) * plane + (size_t)yi * nx, bx,
+                   nx, c[cz * 4 + cy * 2], c[cz * 4 + cy * 2 + 1]);
+          continue;
+        }
 #pragma unroll
         for (int cx = 0; cx < 2; cx++) {
           const int xi = bx + cx;
@@ -201,8 +239,16 @@ int cs_bwd_matched(float* vol_acc, int nx, int ny, int nz, int z_lo,
   int rc = upload_geometry(geom, n_a, s, &dgeom);
   if (rc) return rc;
   const dim3 grid((n_u + 15) / 16, (n_v + 7) / 8, n_a);
-  bwd_matched_kernel<<<grid, 128, 0, s>>>(vol_acc, dgeom, G, step_max, z_lo,
-                                          z_hi, n_u, n_v, proj);
+  // vector reductions need 16-byte aligned rows
+  static const char* knob = getenv("CS_MATCHED_SCALAR");
+  const bool v4 = (nx % 4 == 0) && (((uintptr_t)vol_acc & 15) == 0) &&
+                  !(knob && knob[0] == '1');
+  if (v4)
+    bwd_matched_kernel<true><<<grid, 128, 0, s>>>(vol_acc, dgeom, G, step_max,
+                                                  z_lo, z_hi, n_u, n_v, proj);
+  else
+    bwd_matched_kernel<false><<<grid, 128, 0, s>>>(
+        vol_acc, dgeom, G, step_max, z_lo, z_hi, n_u, n_v, proj);
   cudaError_t e = cudaGetLastError();
   release_geometry(dgeom, s);
   CS_CHECK_CUDA(e);

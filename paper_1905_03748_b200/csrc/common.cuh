@@ -213,10 +213,18 @@ __device__ __forceinline__ float4 gather_a2d(cudaTextureObject_t t, int layer,
 struct LayeredTexture {
   cudaArray_t array = nullptr;
   cudaTextureObject_t tex = 0;
+  cudaSurfaceObject_t surf = 0;
   int w = 0, h = 0, layers = 0;
 };
 
+// TEX_VOLUME: a volume slab as z-layers (x, y per layer);
+// TEX_PROJ: a projection stack as angle-layers (u, v per layer).
 enum TexRole { TEX_VOLUME = 0, TEX_PROJ = 1 };
+
+// Cached (w, h, >= layers) surface-writable layered array, contents
+// undefined; stream-ordered reuse per (device, stream, role).
+int acquire_layered(TexRole role, int w, int h, int layers, cudaStream_t s,
+                    LayeredTexture** out);
 
 // Returns a texture whose array is (w, h, >= layers) and loads `layers`
 // layers from the linear array `src` ([layers][h][w], device or host

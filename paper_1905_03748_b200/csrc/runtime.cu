@@ -61,13 +61,14 @@ std::map<Key, LayeredTexture> g_cache;
 int make_texture(LayeredTexture& t, int w, int h, int layers) {
   cudaChannelFormatDesc fd = cudaCreateChannelDesc<float>();
   cudaExtent ext = make_cudaExtent(w, h, layers);
-  CS_CHECK_CUDA(cudaMalloc3DArray(&t.array, &fd, ext, cudaArrayLayered));
+  CS_CHECK_CUDA(cudaMalloc3DArray(&t.array, &fd, ext,
+                                  cudaArrayLayered | cudaArraySurfaceLoadStore));
   cudaResourceDesc rd = {};
   rd.resType = cudaResourceTypeArray;
   rd.res.array.array = t.array;
   cudaTextureDesc td = {};
-  td.addressMode[0] = cudaAddressModeBorder;  // zero padding in x / u
-  td.addressMode[1] = cudaAddressModeBorder;  // zero padding in y / v
+  td.addressMode[0] = cudaAddressModeBorder;  // zero padding
+  td.addressMode[1] = cudaAddressModeBorder;
   td.addressMode[2] = cudaAddressModeBorder;
   td.borderColor[0] = td.borderColor[1] = td.borderColor[2] =
       td.borderColor[3] = 0.f;
@@ -75,6 +76,7 @@ int make_texture(LayeredTexture& t, int w, int h, int layers) {
   td.readMode = cudaReadModeElementType;
   td.normalizedCoords = 0;
   CS_CHECK_CUDA(cudaCreateTextureObject(&t.tex, &rd, &td, nullptr));
+  CS_CHECK_CUDA(cudaCreateSurfaceObject(&t.surf, &rd));
   t.w = w;
   t.h = h;
   t.layers = layers;
@@ -82,8 +84,8 @@ int make_texture(LayeredTexture& t, int w, int h, int layers) {
 }
 }  // namespace
 
-int load_layered(TexRole role, const float* src, int w, int h, int layers,
-                 cudaStream_t s, LayeredTexture** out) {
+int acquire_layered(TexRole role, int w, int h, int layers, cudaStream_t s,
+                    LayeredTexture** out) {
   CS_REQUIRE(layers >= 1 && layers <= max_layers(), CS_ERR_ARG,
              "layered texture: %d layers outside [1, %d]", layers,
              max_layers());
@@ -95,6 +97,7 @@ int load_layered(TexRole role, const float* src, int w, int h, int layers,
     // shape change: previous launches on this stream may still read the old
     // array, so drain the stream before releasing it.
     CS_CHECK_CUDA(cudaStreamSynchronize(s));
+    cudaDestroySurfaceObject(t.surf);
     cudaDestroyTextureObject(t.tex);
     cudaFreeArray(t.array);
     t = LayeredTexture();
@@ -103,13 +106,20 @@ int load_layered(TexRole role, const float* src, int w, int h, int layers,
     int rc = make_texture(t, w, h, layers);
     if (rc) return rc;
   }
+  *out = &t;
+  return CS_OK;
+}
+
+int load_layered(TexRole role, const float* src, int w, int h, int layers,
+                 cudaStream_t s, LayeredTexture** out) {
+  int rc = acquire_layered(role, w, h, layers, s, out);
+  if (rc) return rc;
   cudaMemcpy3DParms p = {};
   p.srcPtr = make_cudaPitchedPtr((void*)src, (size_t)w * sizeof(float), w, h);
-  p.dstArray = t.array;
+  p.dstArray = (*out)->array;
   p.extent = make_cudaExtent(w, h, layers);
   p.kind = cudaMemcpyDefault;
   CS_CHECK_CUDA(cudaMemcpy3DAsync(&p, s));
-  *out = &t;
   return CS_OK;
 }
 
