@@ -56,12 +56,52 @@ __device__ __forceinline__ void red_pair(float* row, int bx, int nx, float c0,
   if (bx + 1 >= 0 && bx + 1 < nx) red_add(row + bx + 1, c1);
 }
 
+// Per-thread write-combining window in shared memory: a ray's taps land in
+// the 2 (z) x 2 (y) x 8 (x) voxels around its current cell, addressed
+// circularly (slot = ((z & 1) * 2 + (y & 1)) * 8 + (x & 7)) so the window
+// slides with the ray without moving data.  A row segment is flushed to
+// global memory -- one 16-byte vector reduction per aligned x-quad -- only
+// when the ray leaves it: along x every 4 planes, along y / z when the
+// cell's row changes.  This cuts L2 reduction requests ~3x against
+// flushing every cell (the measured limiter: lts tag lookups ~77%).
+// Layout [slot][thread]: every lane owns its own bank (conflict-free).
+constexpr int MW_SLOTS = 32;
+constexpr int MW_THREADS = 128;
+
 template <bool V4>
-__global__ void __launch_bounds__(128)
+__device__ __forceinline__ void mw_flush_quad(float* my, float* vol, int gx,
+                                              int y, int z, int nx, int ny,
+                                              int z_lo, int z_hi,
+                                              size_t plane) {
+  const int base = (((z & 1) << 1) | (y & 1)) * 8 + (gx & 7);
+  float q[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    q[i] = my[(base + i) * MW_THREADS];
+    my[(base + i) * MW_THREADS] = 0.f;
+  }
+  if (q[0] == 0.f && q[1] == 0.f && q[2] == 0.f && q[3] == 0.f) return;
+  if (z < z_lo || z >= z_hi || y < 0 || y >= ny) return;  // masked taps
+  float* row = vol + (size_t)(z - z_lo) * plane + (size_t)y * nx;
+  if (V4 && gx >= 0 && gx + 3 < nx) {
+    red_add4(row + gx, q[0], q[1], q[2], q[3]);
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const int x = gx + i;
+    if (x >= 0 && x < nx && q[i] != 0.f) red_add(row + x, q[i]);
+  }
+}
+
+template <bool V4>
+__global__ void __launch_bounds__(MW_THREADS)
     bwd_matched_kernel(float* __restrict__ vol,
                        const AngleGeom* __restrict__ geom, Grid G,
                        double step_max, int z_lo, int z_hi, int n_u, int n_v,
                        const float* __restrict__ proj) {
+  extern __shared__ float mw_win[];
+  float* my = mw_win + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int u = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
   const int v = blockIdx.y * 8 + (warp >> 1) * 4 + (lane >> 3);
@@ -77,42 +117,26 @@ __global__ void __launch_bounds__(128)
   long long k0l, k1l;
   slab_k_range(r, m, G, z_lo, z_hi, k0l, k1l);
   const int k0 = (int)k0l, k1 = (int)k1l, kc = (int)m.kc;
+  if (k0 >= k1) return;
   const int nx = G.n[0], ny = G.n[1];
   const size_t plane = (size_t)nx * ny;
   const float scaled = val * (float)r.step;
+#pragma unroll
+  for (int i = 0; i < MW_SLOTS; i++) my[i * MW_THREADS] = 0.f;
 
-  // Register-merged corner weights for the current base voxel.
-  int bx = INT_MIN, by = 0, bz = 0;
-  float c[8];
-#pragma unroll
-  for (int i = 0; i < 8; i++) c[i] = 0.f;
-
-  auto flush = [&]() {
-    if (bx == INT_MIN) return;
-#pragma unroll
-    for (int cz = 0; cz < 2; cz++) {
-      const int zi = bz + cz;
-      if (zi < z_lo || zi >= z_hi) continue;
-#pragma unroll
-      for (int cy = 0; cy < 2; cy++) {
-        const int yi = by + cy;
-        if (yi < 0 || yi >= ny) continue;
-        if (V4) {
-          red_pair(vol + (size_t)(zi - z_lo) * plane + (size_t)yi * nx, bx,
-                   nx, c[cz * 4 + cy * 2], c[cz * 4 + cy * 2 + 1]);
-          continue;
-        }
-#pragma unroll
-        for (int cx = 0; cx < 2; cx++) {
-          const int xi = bx + cx;
-          if (xi < 0 || xi >= nx) continue;
-          red_add(vol + (size_t)(zi - z_lo) * plane + (size_t)yi * nx + xi,
-                  c[cz * 4 + cy * 2 + cx]);
-        }
-      }
-    }
+  auto flush_row = [&](int xa, int y, int z) {
+    mw_flush_quad<V4>(my, vol, xa, y, z, nx, ny, z_lo, z_hi, plane);
+    mw_flush_quad<V4>(my, vol, xa + 4, y, z, nx, ny, z_lo, z_hi, plane);
   };
-
+  auto flush_xquad = [&](int gx, int ya, int za) {
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+      mw_flush_quad<V4>(my, vol, gx, ya + (i & 1), za + (i >> 1), nx, ny,
+                        z_lo, z_hi, plane);
+  };
+  const bool x_up = m.B[0] >= 0.f;
+  int xa = 0, ya = 0, za = 0;  // window base
+  bool started = false;
   for (int k = k0; k < k1; ++k) {
     const float kf = (float)(k - kc);
     const float qx = fmaf(kf, m.B[0], m.A[0]);
@@ -121,27 +145,54 @@ __global__ void __launch_bounds__(128)
     const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
     const float wx = qx - fx, wy = qy - fy, wz = qz - fz;
     const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
-    if (ix != bx || iy != by || iz != bz) {
-      flush();
-      bx = ix;
-      by = iy;
-      bz = iz;
-#pragma unroll
-      for (int i = 0; i < 8; i++) c[i] = 0.f;
+    if (!started) {
+      xa = x_up ? (ix & ~3) : (((ix + 1) & ~3) - 4);
+      ya = iy;
+      za = iz;
+      started = true;
+    } else {
+      // the sample step is <= half a voxel: cells move by <= 1 per axis
+      if (iz != za) {
+        const int zo = iz > za ? za : za + 1;  // plane the ray left
+        flush_row(xa, ya, zo);
+        flush_row(xa, ya + 1, zo);
+        za = iz;
+      }
+      if (iy != ya) {
+        const int yo = iy > ya ? ya : ya + 1;
+        flush_row(xa, yo, za);
+        flush_row(xa, yo, za + 1);
+        ya = iy;
+      }
+      if (ix + 1 >= xa + 8) {
+        flush_xquad(xa, ya, za);
+        xa += 4;
+      } else if (ix < xa) {
+        flush_xquad(xa + 4, ya, za);
+        xa -= 4;
+      }
     }
     const float z0 = scaled * (1.f - wz), z1 = scaled * wz;
-    const float y00 = z0 * (1.f - wy), y01 = z0 * wy;
-    const float y10 = z1 * (1.f - wy), y11 = z1 * wy;
-    c[0] = fmaf(y00, 1.f - wx, c[0]);
-    c[1] = fmaf(y00, wx, c[1]);
-    c[2] = fmaf(y01, 1.f - wx, c[2]);
-    c[3] = fmaf(y01, wx, c[3]);
-    c[4] = fmaf(y10, 1.f - wx, c[4]);
-    c[5] = fmaf(y10, wx, c[5]);
-    c[6] = fmaf(y11, 1.f - wx, c[6]);
-    c[7] = fmaf(y11, wx, c[7]);
+    const float w00 = z0 * (1.f - wy), w01 = z0 * wy;
+    const float w10 = z1 * (1.f - wy), w11 = z1 * wy;
+    const int x0 = ix & 7, x1 = (ix + 1) & 7;
+    const int r00 = (((iz & 1) << 1) | (iy & 1)) * 8;
+    const int r01 = r00 ^ 8;   // y + 1 flips the y parity bit
+    const int r10 = r00 ^ 16;  // z + 1 flips the z parity bit
+    const int r11 = r00 ^ 24;
+    my[(r00 + x0) * MW_THREADS] += w00 * (1.f - wx);
+    my[(r00 + x1) * MW_THREADS] += w00 * wx;
+    my[(r01 + x0) * MW_THREADS] += w01 * (1.f - wx);
+    my[(r01 + x1) * MW_THREADS] += w01 * wx;
+    my[(r10 + x0) * MW_THREADS] += w10 * (1.f - wx);
+    my[(r10 + x1) * MW_THREADS] += w10 * wx;
+    my[(r11 + x0) * MW_THREADS] += w11 * (1.f - wx);
+    my[(r11 + x1) * MW_THREADS] += w11 * wx;
   }
-  flush();
+  flush_row(xa, ya, za);
+  flush_row(xa, ya + 1, za);
+  flush_row(xa, ya, za + 1);
+  flush_row(xa, ya + 1, za + 1);
 }
 
 constexpr int FDK_ZB = 16;  // z voxels per thread (registers)
@@ -243,11 +294,12 @@ int cs_bwd_matched(float* vol_acc, int nx, int ny, int nz, int z_lo,
   static const char* knob = getenv("CS_MATCHED_SCALAR");
   const bool v4 = (nx % 4 == 0) && (((uintptr_t)vol_acc & 15) == 0) &&
                   !(knob && knob[0] == '1');
+  const size_t smem = sizeof(float) * MW_SLOTS * MW_THREADS;
   if (v4)
-    bwd_matched_kernel<true><<<grid, 128, 0, s>>>(vol_acc, dgeom, G, step_max,
-                                                  z_lo, z_hi, n_u, n_v, proj);
+    bwd_matched_kernel<true><<<grid, MW_THREADS, smem, s>>>(
+        vol_acc, dgeom, G, step_max, z_lo, z_hi, n_u, n_v, proj);
   else
-    bwd_matched_kernel<false><<<grid, 128, 0, s>>>(
+    bwd_matched_kernel<false><<<grid, MW_THREADS, smem, s>>>(
         vol_acc, dgeom, G, step_max, z_lo, z_hi, n_u, n_v, proj);
   cudaError_t e = cudaGetLastError();
   release_geometry(dgeom, s);
