@@ -501,12 +501,14 @@ def _flush(pending, out, only_buf):
     pending[:] = keep
 
 
-def _gather_slabs(out, slabs, queues, rank, on_dev):
+def _gather_slabs(out, slabs, queues, rank, on_dev, device=None):
     """Every rank ends with the full volume: broadcast each slab from its
-    owner (NCCL over NVLink between ranks)."""
+    owner (NCCL over NVLink between ranks; ``device`` is where host volumes
+    are staged for the collective, default the current GPU)."""
     import torch.distributed as dist
-    dev = torch.device("cuda", torch.cuda.current_device())
-    full = out if on_dev else torch.from_numpy(out).to(dev)
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    full = out if on_dev else torch.from_numpy(out).to(device)
     for owner, q in enumerate(queues):
         for si in q:
             z0, z1 = slabs[si]

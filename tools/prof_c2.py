@@ -1,5 +1,6 @@
-"""Run each hot kernel at config 2 (512^3, 512^2, 360 angles) twice (warm
-+ profiled) for ncu: fwd_interp, bwd_matched, bwd_fdk, tv step."""
+"""Replays the bench's launches at config 2 (512^3, 512^2, 360 views) for
+ncu: each hot kernel launched on its first CHUNK-view chunk exactly as
+bench.py launches it (warm-up launch first, then the profiled one)."""
 import os
 import sys
 
@@ -10,8 +11,9 @@ import bench
 import paper_1905_03748_b200 as cs
 from paper_1905_03748_b200 import kernels as K
 
-n = int(os.environ.get("PROF_N", 512))
-A = int(os.environ.get("PROF_A", 360))
+n = int(os.environ.get("PROF_N", bench.N_VOX))
+A = int(os.environ.get("PROF_A", bench.N_ANG))
+C = int(os.environ.get("PROF_CHUNK", bench.CHUNK))
 which = os.environ.get("PROF_KERNELS", "fwd,matched,fdk").split(",")
 g = bench.make_geometry(n, A, cs)
 dev = torch.device("cuda", 0)
@@ -19,12 +21,14 @@ vol = cs.phantom(cs.PhantomKind.SHEPP_LOGAN_3D, g.voxel_grid, device=dev).data
 y = torch.empty((A, n, n), device=dev)
 K.fwd_interp(vol, g, (0, A), (0, n), y)
 acc = torch.zeros((n, n, n), device=dev)
+proj = torch.empty((C, n, n), device=dev)
+torch.cuda.synchronize()
 for rep in range(2):
     if "fwd" in which:
-        K.fwd_interp(vol, g, (0, A), (0, n), y)
+        K.fwd_interp(vol, g, (0, C), (0, n), proj)
     if "matched" in which:
-        K.bwd_matched(y, g, (0, A), (0, n), acc)
+        K.bwd_matched(y[0:C], g, (0, C), (0, n), acc)
     if "fdk" in which:
-        K.bwd_fdk(y, g, (0, A), (0, n), acc)
+        K.bwd_fdk(y[0:C], g, (0, C), (0, n), acc)
 torch.cuda.synchronize()
 print("done")
