@@ -375,6 +375,20 @@ def run_extras(args, cs, K, g, vol, y, dev, rank, world, arange, zrange):
     torch.cuda.synchronize()
     out["atb_fdk_gups"] = reps * float(A) * (z1 - z0) * n * n / (
         s.elapsed_time(e) * 1e-3) / 1e9
+    # matched Atb on a dense (no zero pixels) stack: the bench input Ax(phantom)
+    # has zeros outside the head's shadow, which the reference skips too
+    # (_kernels.py:295-296); a residual stack is dense
+    dense = torch.randn(y.shape, device=dev, generator=torch.Generator(
+        device=dev).manual_seed(1))
+    K.bwd_matched(dense, g, (0, A), zrange, slab)
+    torch.cuda.synchronize()
+    s.record()
+    K.bwd_matched(dense, g, (0, A), zrange, slab)
+    e.record()
+    torch.cuda.synchronize()
+    out["atb_matched_dense_gups"] = float(A) * (z1 - z0) * n * n / (
+        s.elapsed_time(e) * 1e-3) / 1e9
+    del dense
 
     # end-to-end through the public API with pinned host buffers:
     # Ax(volume host) -> projections host; Atb(projections host) -> slab host

@@ -285,6 +285,11 @@ int cs_bwd_matched(float* vol_acc, int nx, int ny, int nz, int z_lo,
              "bad projection shape");
   CS_REQUIRE(step_max > 0.0, CS_ERR_ARG, "step_max must be positive");
   cudaStream_t s = (cudaStream_t)stream;
+  static const char* staged_knob = getenv("CS_MATCHED_WINDOW");
+  if (!(staged_knob && staged_knob[0] == '1'))  // production: staged boxes
+    return launch_staged<OP_BWD, 0>(nullptr, vol_acc, nx, ny, nz, z_lo, z_hi,
+                                    grid6, geom, n_a, n_u, n_v, step_max,
+                                    nullptr, proj, nullptr, nullptr, s);
   const Grid G = make_grid(grid6, nx, ny, nz);
   AngleGeom* dgeom = nullptr;
   int rc = upload_geometry(geom, n_a, s, &dgeom);

@@ -242,6 +242,15 @@ void release_geometry(AngleGeom* d_geom, cudaStream_t s);
 
 Grid make_grid(const double grid6[6], int nx, int ny, int nz);
 
+// Shared-memory staged Ax / matched Atb (staged.cu).
+enum StOpKind { OP_FWD = 0, OP_BWD = 1 };
+template <int OP, int MODE>
+int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
+                  int z_lo, int z_hi, const double* grid6, const double* geom,
+                  int n_a, int n_u, int n_v, double step_max, float* out,
+                  const float* proj_in, const float* rb, const float* rw,
+                  cudaStream_t s);
+
 inline int num_sms() {
   static int sms = -1;
   if (sms < 0) {

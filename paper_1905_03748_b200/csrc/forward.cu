@@ -14,6 +14,8 @@
 // x/y; z taps are masked to the slab [z_lo, z_hi) exactly as
 // _kernels.py:259-262, and the sample range is clipped to the slab so a
 // slab launch costs only its share of the ray.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cs {
@@ -185,6 +187,14 @@ static int launch_interp(const float* vol, int nx, int ny, int nz, int z_lo,
   int rc = check_common(nx, ny, nz, z_lo, z_hi, n_a, n_u, n_v);
   if (rc) return rc;
   CS_REQUIRE(step_max > 0.0, CS_ERR_ARG, "step_max must be positive");
+  // Texture-gather kernel (below) is the production Ax; the shared-memory
+  // staged variant (staged.cu) is selectable for A/B runs (CS_FWD_STAGED=1):
+  // it is latency-bound on its box loads (149 vs 284 GUPS at config 2, r01).
+  static const char* knob = getenv("CS_FWD_STAGED");
+  if (knob && knob[0] == '1')
+    return launch_staged<OP_FWD, MODE>(vol, nullptr, nx, ny, nz, z_lo, z_hi,
+                                       grid6, geom, n_a, n_u, n_v, step_max,
+                                       out, nullptr, b, w, s);
   const Grid G = make_grid(grid6, nx, ny, nz);
   AngleGeom* dgeom = nullptr;
   if ((rc = upload_geometry(geom, n_a, s, &dgeom))) return rc;

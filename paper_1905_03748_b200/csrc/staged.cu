@@ -1,0 +1,548 @@
+// staged.cu -- shared-memory staged Ax (K1) and matched Atb (K2).
+//
+// A CTA owns a 32 (u) x 8 (v) tile of detector rays of ONE view; warp w is
+// detector row v0 + w, lane l is pixel u0 + l.  The view's rays travel
+// mainly along M = x or y (|d_M| >= |d_T|); the CTA walks the volume in
+// chunks of ST_S planes along M.  For each chunk it computes the box of
+// voxels its rays' trilinear supports touch (block min/max of the first /
+// last sample of every ray in the chunk) and stages that box in shared
+// memory:
+//   * Ax (OP_FWD): the box is loaded from the fp32 slab (zero outside the
+//     grid / slab = the reference's masks, _kernels.py:259-272), then every
+//     ray samples its chunk from shared memory -- 8 LDS per sample instead of
+//     2 texture gathers, lifting the texture-writeback ceiling of the tex
+//     kernel (forward.cu);
+//   * matched Atb (OP_BWD): the box is zeroed, rays deposit their 8 taps
+//     with native int32 shared atomics (ATOMS.ADD; fp32 shared atomics are
+//     CAS loops on sm_100) in fixed point, scaled per CTA by its largest
+//     |proj| so no voxel sum can overflow; the box is then added to global
+//     memory with one 16-byte RED per aligned x-quad.
+// Samples, weights and masks are exactly those of the tex / register
+// kernels (same fp64 ray set-up, same fp32 lattice q(k) = A + (k - kc) B),
+// so chunking changes only summation order.  Boxes that would not fit the
+// shared-memory budget are served from global memory for that chunk.
+#include "common.cuh"
+
+namespace cs {
+
+constexpr int ST_TU = 32;
+constexpr int ST_TV = 8;
+constexpr int ST_THREADS = ST_TU * ST_TV;
+constexpr int ST_S = 8;  // planes per chunk along the main axis
+
+
+__device__ __forceinline__ int qfloor(const March& m, int k, int axis) {
+  return (int)floorf(fmaf((float)(k - (int)m.kc), m.B[axis], m.A[axis]));
+}
+
+// i -> (x, y, z) in a box [bz][by][bx] without integer division: float
+// reciprocal estimate + one correction step (i < 2^24).
+__device__ __forceinline__ void box_coords(int i, int bx, int bxy, float inv_bx,
+                                           float inv_bxy, int& x, int& y,
+                                           int& z) {
+  z = (int)((float)i * inv_bxy);
+  int rem = i - z * bxy;
+  if (rem < 0) {
+    z--;
+    rem += bxy;
+  } else if (rem >= bxy) {
+    z++;
+    rem -= bxy;
+  }
+  y = (int)((float)rem * inv_bx);
+  x = rem - y * bx;
+  if (x < 0) {
+    y--;
+    x += bx;
+  } else if (x >= bx) {
+    y++;
+    x -= bx;
+  }
+}
+
+// Red of a float4 quad (16-byte aligned) -- see backward.cu.
+__device__ __forceinline__ void st_red4(float* p, float a, float b, float c,
+                                        float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p),
+               "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+template <int OP, int M, int MODE>
+__global__ void __launch_bounds__(ST_THREADS, 3)
+    staged_kernel(const float* __restrict__ vol_in, float* __restrict__ vol_acc,
+                  const AngleGeom* __restrict__ geom,
+                  const int* __restrict__ view_ids, Grid G, double step_max,
+                  int z_lo, int z_hi, int n_u, int n_v,
+                  float* __restrict__ out, const float* __restrict__ proj_in,
+                  const float* __restrict__ rb, const float* __restrict__ rw,
+                  int box_cap, float fx_budget, int vec_ok) {
+  constexpr int T = 1 - M;
+  extern __shared__ float st_box[];
+  int* box_i = reinterpret_cast<int*>(st_box);
+  __shared__ int ext[8];  // mlo, mhi, tlo, thi, zlo, zhi, dir-flags
+  __shared__ float s_scale;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int u = blockIdx.x * ST_TU + lane;
+  const int v = blockIdx.y * ST_TV + warp;
+  const int a = view_ids[blockIdx.z];
+  const bool valid = u < n_u && v < n_v;
+  const int nx = G.n[0], ny = G.n[1];
+  const size_t plane = (size_t)nx * ny;
+  const size_t pix = ((size_t)a * n_v + v) * n_u + u;
+
+  float val = 0.f;
+  if (OP == OP_BWD && valid) val = __ldg(proj_in + pix);
+  Ray r;
+  r.n = 0;
+  r.step = 0.0;
+  if (valid && (OP == OP_FWD || val != 0.f)) setup_ray(geom[a], G, step_max, u, v, r);
+  March m;
+  int k0 = 0, k1 = 0;
+  if (r.n > 0) {
+    march_params(r, G, m);
+    long long k0l, k1l;
+    slab_k_range(r, m, G, z_lo, z_hi, k0l, k1l);
+    k0 = (int)k0l;
+    k1 = (int)k1l;
+  }
+  const bool has = k1 > k0;
+
+  if (threadIdx.x == 0) {
+    ext[0] = INT_MAX;
+    ext[1] = INT_MIN;
+    ext[6] = 0;  // any ray marching -M
+    ext[7] = 0;  // any ray marching +M
+    s_scale = 0.f;
+  }
+  __syncthreads();
+  if (has) {
+    const int fa = qfloor(m, k0, M), fb = qfloor(m, k1 - 1, M);
+    atomicMin(&ext[0], min(fa, fb));
+    atomicMax(&ext[1], max(fa, fb));
+    atomicOr(&ext[m.B[M] >= 0.f ? 7 : 6], 1);
+  }
+  if (OP == OP_BWD) {
+    // per-CTA fixed-point scale: taps are |val| * step * w, w <= 1
+    const float mag = has ? fabsf(val) * (float)r.step : 0.f;
+    float wmax = mag;
+    for (int o = 16; o > 0; o >>= 1)
+      wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    if (lane == 0) atomicMax(reinterpret_cast<int*>(&s_scale),
+                             __float_as_int(wmax));  // non-negative floats
+  }
+  __syncthreads();
+  const int mlo = ext[0], mhi = ext[1];
+  if (mlo > mhi) {  // no ray of the tile touches the slab
+    if (OP == OP_FWD && valid) {
+      if (MODE == 0)
+        out[pix] = 0.f;
+      else if (MODE == 2)
+        out[pix] = (rw ? rw[pix] : 1.f) * rb[pix];
+    }
+    return;
+  }
+  const int dir = ext[6] ? -1 : 1;  // march direction (uniform per view)
+  const bool mixed = ext[6] && ext[7];
+  float fscale = 0.f, inv_scale = 0.f;
+  if (OP == OP_BWD) {
+    const float tmax = s_scale;
+    fscale = tmax > 0.f ? fx_budget / tmax : 0.f;
+    inv_scale = fscale > 0.f ? 1.f / fscale : 0.f;
+  }
+  const float sv = OP == OP_BWD ? val * (float)r.step * fscale : 0.f;
+
+  float acc = 0.f;
+  if (mixed) {
+    // rays of this tile march both ways along M (degenerate geometry):
+    // serve every sample from global memory, no staging
+    for (int kk = k0; kk < k1; kk++) {
+      const float kf = (float)(kk - (int)m.kc);
+      const float qx = fmaf(kf, m.B[0], m.A[0]);
+      const float qy = fmaf(kf, m.B[1], m.A[1]);
+      const float qz = fmaf(kf, m.B[2], m.A[2]);
+      const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
+      const float wx = qx - fx, wy = qy - fy, wz = qz - fz;
+      const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
+#pragma unroll
+      for (int cz = 0; cz < 2; cz++) {
+        const int zi = iz + cz;
+        if (zi < z_lo || zi >= z_hi) continue;
+        const float fz_ = cz ? wz : 1.f - wz;
+#pragma unroll
+        for (int cy = 0; cy < 2; cy++) {
+          const int yi = iy + cy;
+          if (yi < 0 || yi >= ny) continue;
+          const float fy_ = cy ? wy : 1.f - wy;
+#pragma unroll
+          for (int cx = 0; cx < 2; cx++) {
+            const int xi = ix + cx;
+            if (xi < 0 || xi >= nx) continue;
+            const float w = fz_ * fy_ * (cx ? wx : 1.f - wx);
+            const size_t gi = (size_t)(zi - z_lo) * plane + (size_t)yi * nx + xi;
+            if (OP == OP_FWD)
+              acc = fmaf(w, __ldg(vol_in + gi), acc);
+            else
+              atomicAdd(vol_acc + gi, val * (float)r.step * w);
+          }
+        }
+      }
+    }
+  }
+  // samples are consumed in index order in both march directions: chunk c
+  // takes the next run of samples whose M-cell lies in it
+  int k = k0;
+  const int n_chunks = mixed ? 0 : (mhi - mlo) / ST_S + 1;
+  for (int c = 0; c < n_chunks; c++) {
+    // chunk = M-cells [c_lo, c_hi] in march order
+    const int c_lo = dir > 0 ? mlo + c * ST_S : mhi - c * ST_S - ST_S + 1;
+    const int c_hi = c_lo + ST_S - 1;
+    const int ka = k;
+    int kb = k;
+    if (has) {
+      // last sample of the chunk: qM(k) crosses the chunk's far face at
+      // k* = kc + (face - A_M) / B_M; estimate, then settle on the exact
+      // fp32 cell test (the same floor the sampling loop uses)
+      const float face = dir > 0 ? (float)(c_hi + 1) : (float)c_lo;
+      const float kst = (face - m.A[M]) / m.B[M] + (float)(int)m.kc;
+      int ke = (int)fminf(fmaxf(ceilf(kst), (float)k), (float)k1);
+      if (dir > 0) {
+        while (ke > k && qfloor(m, ke - 1, M) > c_hi) ke--;
+        while (ke < k1 && qfloor(m, ke, M) <= c_hi) ke++;
+      } else {
+        while (ke > k && qfloor(m, ke - 1, M) < c_lo) ke--;
+        while (ke < k1 && qfloor(m, ke, M) >= c_lo) ke++;
+      }
+      kb = ke;
+      k = kb;
+    }
+    const bool any = kb > ka;
+    __syncthreads();  // previous chunk's box fully consumed
+    if (threadIdx.x == 0) {
+      ext[2] = INT_MAX;
+      ext[3] = INT_MIN;
+      ext[4] = INT_MAX;
+      ext[5] = INT_MIN;
+    }
+    __syncthreads();
+    if (any) {
+      const int t0 = qfloor(m, ka, T), t1 = qfloor(m, kb - 1, T);
+      const int zz0 = qfloor(m, ka, 2), zz1 = qfloor(m, kb - 1, 2);
+      atomicMin(&ext[2], min(t0, t1));
+      atomicMax(&ext[3], max(t0, t1));
+      atomicMin(&ext[4], min(zz0, zz1));
+      atomicMax(&ext[5], max(zz0, zz1));
+    }
+    __syncthreads();
+    if (ext[2] > ext[3] && !mixed) continue;  // nobody samples this chunk
+    // box over taps: cells [lo, hi + 1] per axis; x padded to aligned quads
+    int bo[3], bn[3];
+    bo[M] = c_lo;
+    bn[M] = ST_S + 1;
+    bo[T] = ext[2];
+    bn[T] = ext[3] - ext[2] + 2;
+    bo[2] = ext[4];
+    bn[2] = ext[5] - ext[4] + 2;
+    {
+      const int x0 = bo[0] & ~3;
+      bn[0] = ((bo[0] + bn[0] - x0) + 3) & ~3;
+      bo[0] = x0;
+    }
+    const int bxy = bn[0] * bn[1];
+    const int bsize = bxy * bn[2];
+    const float inv_bx = 1.f / (float)bn[0], inv_bxy = 1.f / (float)bxy;
+    const bool fits = !mixed && bsize <= box_cap;
+
+    if (fits) {
+      if (OP == OP_FWD) {
+        // one aligned float4 per thread and step: rows of bn[0] / 4 quads
+        const int qpr = bn[0] >> 2;
+        const int nquads = qpr * bn[1] * bn[2];
+        const float inv_q = 1.f / (float)qpr, inv_y = 1.f / (float)bn[1];
+        for (int qi = threadIdx.x; qi < nquads; qi += ST_THREADS) {
+          int row = (int)((float)qi * inv_q);
+          int xq = qi - row * qpr;
+          if (xq < 0) { row--; xq += qpr; } else if (xq >= qpr) { row++; xq -= qpr; }
+          int bz = (int)((float)row * inv_y);
+          int by = row - bz * bn[1];
+          if (by < 0) { bz--; by += bn[1]; } else if (by >= bn[1]) { bz++; by -= bn[1]; }
+          const int gx = bo[0] + 4 * xq, gy = bo[1] + by, gz = bo[2] + bz;
+          float4 q4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (gy >= 0 && gy < ny && gz >= z_lo && gz < z_hi) {
+            const float* src = vol_in + (size_t)(gz - z_lo) * plane +
+                               (size_t)gy * nx;
+            if (vec_ok && gx >= 0 && gx + 3 < nx) {
+              q4 = __ldg(reinterpret_cast<const float4*>(src + gx));
+            } else {
+              if (gx >= 0 && gx < nx) q4.x = __ldg(src + gx);
+              if (gx + 1 >= 0 && gx + 1 < nx) q4.y = __ldg(src + gx + 1);
+              if (gx + 2 >= 0 && gx + 2 < nx) q4.z = __ldg(src + gx + 2);
+              if (gx + 3 >= 0 && gx + 3 < nx) q4.w = __ldg(src + gx + 3);
+            }
+          }
+          *reinterpret_cast<float4*>(st_box + row * bn[0] + 4 * xq) = q4;
+        }
+      } else {
+        for (int i = threadIdx.x; i < bsize; i += ST_THREADS) box_i[i] = 0;
+      }
+      __syncthreads();
+    }
+    // ---- samples of the chunk
+    if (any) {
+      for (int kk = ka; kk < kb; kk++) {
+        const float kf = (float)(kk - (int)m.kc);
+        const float qx = fmaf(kf, m.B[0], m.A[0]);
+        const float qy = fmaf(kf, m.B[1], m.A[1]);
+        const float qz = fmaf(kf, m.B[2], m.A[2]);
+        const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
+        const float wx = qx - fx, wy = qy - fy, wz = qz - fz;
+        const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
+        if (fits) {
+          const int b = ((iz - bo[2]) * bn[1] + (iy - bo[1])) * bn[0] +
+                        (ix - bo[0]);
+          if (OP == OP_FWD) {
+            const float s000 = st_box[b], s001 = st_box[b + 1];
+            const float s010 = st_box[b + bn[0]], s011 = st_box[b + bn[0] + 1];
+            const float s100 = st_box[b + bxy], s101 = st_box[b + bxy + 1];
+            const float s110 = st_box[b + bxy + bn[0]];
+            const float s111 = st_box[b + bxy + bn[0] + 1];
+            const float r00 = fmaf(wx, s001 - s000, s000);
+            const float r01 = fmaf(wx, s011 - s010, s010);
+            const float r10 = fmaf(wx, s101 - s100, s100);
+            const float r11 = fmaf(wx, s111 - s110, s110);
+            const float b0 = fmaf(wy, r01 - r00, r00);
+            const float b1 = fmaf(wy, r11 - r10, r10);
+            acc += fmaf(wz, b1 - b0, b0);
+          } else {
+            const float z0 = sv * (1.f - wz), z1 = sv * wz;
+            const float y00 = z0 * (1.f - wy), y01 = z0 * wy;
+            const float y10 = z1 * (1.f - wy), y11 = z1 * wy;
+            atomicAdd(&box_i[b], __float2int_rn(y00 * (1.f - wx)));
+            atomicAdd(&box_i[b + 1], __float2int_rn(y00 * wx));
+            atomicAdd(&box_i[b + bn[0]], __float2int_rn(y01 * (1.f - wx)));
+            atomicAdd(&box_i[b + bn[0] + 1], __float2int_rn(y01 * wx));
+            atomicAdd(&box_i[b + bxy], __float2int_rn(y10 * (1.f - wx)));
+            atomicAdd(&box_i[b + bxy + 1], __float2int_rn(y10 * wx));
+            atomicAdd(&box_i[b + bxy + bn[0]], __float2int_rn(y11 * (1.f - wx)));
+            atomicAdd(&box_i[b + bxy + bn[0] + 1], __float2int_rn(y11 * wx));
+          }
+        } else {
+          // overflow path: straight from / to global memory
+#pragma unroll
+          for (int cz = 0; cz < 2; cz++) {
+            const int zi = iz + cz;
+            if (zi < z_lo || zi >= z_hi) continue;
+            const float fz_ = cz ? wz : 1.f - wz;
+#pragma unroll
+            for (int cy = 0; cy < 2; cy++) {
+              const int yi = iy + cy;
+              if (yi < 0 || yi >= ny) continue;
+              const float fy_ = cy ? wy : 1.f - wy;
+#pragma unroll
+              for (int cx = 0; cx < 2; cx++) {
+                const int xi = ix + cx;
+                if (xi < 0 || xi >= nx) continue;
+                const float w = fz_ * fy_ * (cx ? wx : 1.f - wx);
+                const size_t gi =
+                    (size_t)(zi - z_lo) * plane + (size_t)yi * nx + xi;
+                if (OP == OP_FWD)
+                  acc = fmaf(w, __ldg(vol_in + gi), acc);
+                else
+                  atomicAdd(vol_acc + gi, val * (float)r.step * w);
+              }
+            }
+          }
+        }
+      }
+    }
+    if (OP == OP_BWD && fits) {
+      __syncthreads();
+      // flush the box: one 16-byte reduction per aligned x-quad
+      const int nq = bsize >> 2;
+      for (int qd = threadIdx.x; qd < nq; qd += ST_THREADS) {
+        const int i = qd << 2;
+        const int4 q = *reinterpret_cast<const int4*>(box_i + i);
+        if ((q.x | q.y | q.z | q.w) == 0) continue;
+        int bx, by, bz;
+        box_coords(i, bn[0], bxy, inv_bx, inv_bxy, bx, by, bz);
+        const int gx = bo[0] + bx, gy = bo[1] + by, gz = bo[2] + bz;
+        if (gy < 0 || gy >= ny || gz < z_lo || gz >= z_hi) continue;
+        float* dst = vol_acc + (size_t)(gz - z_lo) * plane + (size_t)gy * nx;
+        const float f0 = (float)q.x * inv_scale, f1 = (float)q.y * inv_scale;
+        const float f2 = (float)q.z * inv_scale, f3 = (float)q.w * inv_scale;
+        if (vec_ok && gx >= 0 && gx + 3 < nx) {
+          st_red4(dst + gx, f0, f1, f2, f3);
+        } else {
+          const float f[4] = {f0, f1, f2, f3};
+#pragma unroll
+          for (int j = 0; j < 4; j++)
+            if (gx + j >= 0 && gx + j < nx && f[j] != 0.f)
+              atomicAdd(dst + gx + j, f[j]);
+        }
+      }
+    }
+  }
+  if (OP == OP_FWD && valid) {
+    const float outv = acc * (float)r.step;
+    if (MODE == 0)
+      out[pix] = outv;
+    else if (MODE == 1)
+      out[pix] += outv;
+    else
+      out[pix] = (rw ? rw[pix] : 1.f) * (rb[pix] - outv);
+  }
+}
+
+// Main axis of a view from its central ray: 0 = x, 1 = y.
+static int view_axis(const double* g12, int n_u, int n_v) {
+  double d[2];
+  for (int i = 0; i < 2; i++)
+    d[i] = g12[3 + i] + 0.5 * (n_u - 1) * g12[6 + i] +
+           0.5 * (n_v - 1) * g12[9 + i] - g12[i];
+  return fabs(d[0]) >= fabs(d[1]) ? 0 : 1;
+}
+
+// Fixed-point budget for matched deposits: the int32 box must hold the
+// largest per-voxel chunk sum.  A voxel's trilinear support (2 voxels per
+// axis) is crossed by at most (2 / footprint + 1)^2 rays and each ray puts
+// at most (2 / min step + 1) samples of weight <= 1 into it; the footprint
+// of a pixel is smallest nearest the source (magnification dsd / (dso - r)).
+// Returns the scale numerator: per CTA, scale = budget / max|val * step|.
+static float fixed_point_budget(const double* grid6, int nx, int ny, int nz,
+                                const double* geom, int n_a, int n_u, int n_v,
+                                double step_max) {
+  const double ex = nx * grid6[3], ey = ny * grid6[4], ez = nz * grid6[5];
+  const double gc[3] = {grid6[0] + 0.5 * ex, grid6[1] + 0.5 * ey,
+                        grid6[2] + 0.5 * ez};
+  const double rad = 0.5 * sqrt(ex * ex + ey * ey + ez * ez);
+  const double vmax = fmax(grid6[3], fmax(grid6[4], grid6[5]));
+  double fp = 1e300;
+  for (int a = 0; a < n_a; a++) {
+    const double* g = geom + 12 * a;
+    const double du = sqrt(g[6] * g[6] + g[7] * g[7] + g[8] * g[8]);
+    const double dv = sqrt(g[9] * g[9] + g[10] * g[10] + g[11] * g[11]);
+    double c[3], s2c[3];
+    for (int i = 0; i < 3; i++) {
+      c[i] = g[3 + i] + 0.5 * (n_u - 1) * g[6 + i] +
+             0.5 * (n_v - 1) * g[9 + i] - g[i];
+      s2c[i] = gc[i] - g[i];
+    }
+    const double dsd = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+    const double dso = sqrt(s2c[0] * s2c[0] + s2c[1] * s2c[1] + s2c[2] * s2c[2]);
+    const double near = fmax(dso - rad, 1e-6 * dsd);
+    fp = fmin(fp, fmin(du, dv) * near / dsd / vmax);
+  }
+  fp = fmax(fp, 1e-3);
+  const double rays = (2.0 / fp + 1.0) * (2.0 / fp + 1.0);
+  const double samples = 2.0 * vmax / (0.5 * step_max) + 1.0;
+  const double bound = fmin(rays, (double)ST_THREADS) * samples;
+  double b = 1.0e9 / bound;  // per-voxel |sum| <= 1e9 < 2^31
+  if (b > 1.0e8) b = 1.0e8;
+  return (float)b;
+}
+
+}  // namespace cs
+
+using namespace cs;
+
+namespace cs {
+
+static size_t staged_smem_cap() {
+  static size_t cap = 0;
+  if (!cap) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                           dev);
+    cap = optin > 0 ? (size_t)optin : 48 * 1024;
+  }
+  return cap;
+}
+
+// Launch one staged pass over n_a views (OP_FWD: Ax into out with MODE
+// epilogue; OP_BWD: matched Atb into vol_acc).
+template <int OP, int MODE>
+int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
+                  int z_lo, int z_hi, const double* grid6, const double* geom,
+                  int n_a, int n_u, int n_v, double step_max, float* out,
+                  const float* proj_in, const float* rb, const float* rw,
+                  cudaStream_t s) {
+  const Grid G = make_grid(grid6, nx, ny, nz);
+  AngleGeom* dgeom = nullptr;
+  int rc = upload_geometry(geom, n_a, s, &dgeom);
+  if (rc) return rc;
+  int* ids_h = (int*)malloc(sizeof(int) * (size_t)n_a);
+  int nxm = 0;
+  for (int a = 0; a < n_a; a++)
+    if (view_axis(geom + 12 * a, n_u, n_v) == 0) ids_h[nxm++] = a;
+  int nall = nxm;
+  for (int a = 0; a < n_a; a++)
+    if (view_axis(geom + 12 * a, n_u, n_v) == 1) ids_h[nall++] = a;
+  int* ids = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&ids, sizeof(int) * n_a, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(ids, ids_h, sizeof(int) * n_a, cudaMemcpyHostToDevice,
+                        s);
+  free(ids_h);
+  if (e != cudaSuccess) {
+    release_geometry(dgeom, s);
+    CS_CHECK_CUDA(e);
+  }
+  const size_t smem = 64 * 1024;  // 3 CTAs per SM
+  const int cap = (int)(smem / sizeof(float));
+  const float budget =
+      OP == OP_BWD ? fixed_point_budget(grid6, nx, ny, nz, geom, n_a, n_u, n_v,
+                                        step_max)
+                   : 0.f;
+  const void* vbase = OP == OP_BWD ? (const void*)vol_acc : (const void*)vol_in;
+  const int vec_ok = (nx % 4 == 0) && (((uintptr_t)vbase & 15) == 0);
+  const unsigned gx = (n_u + ST_TU - 1) / ST_TU, gy = (n_v + ST_TV - 1) / ST_TV;
+  auto k0 = staged_kernel<OP, 0, MODE>;
+  auto k1 = staged_kernel<OP, 1, MODE>;
+  static bool attr_set = false;  // per process; one device per ordinal
+  if (!attr_set) {
+    cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr_set = true;
+  }
+  if (nxm > 0)
+    k0<<<dim3(gx, gy, nxm), ST_THREADS, smem, s>>>(
+        vol_in, vol_acc, dgeom, ids, G, step_max, z_lo, z_hi, n_u, n_v, out,
+        proj_in, rb, rw, cap, budget, vec_ok);
+  if (nall > nxm)
+    k1<<<dim3(gx, gy, nall - nxm), ST_THREADS, smem, s>>>(
+        vol_in, vol_acc, dgeom, ids + nxm, G, step_max, z_lo, z_hi, n_u, n_v,
+        out, proj_in, rb, rw, cap, budget, vec_ok);
+  e = cudaGetLastError();
+  cudaFreeAsync(ids, s);
+  release_geometry(dgeom, s);
+  CS_CHECK_CUDA(e);
+  (void)staged_smem_cap;
+  return CS_OK;
+}
+
+template int launch_staged<OP_FWD, 0>(const float*, float*, int, int, int,
+                                      int, int, const double*, const double*,
+                                      int, int, int, double, float*,
+                                      const float*, const float*,
+                                      const float*, cudaStream_t);
+template int launch_staged<OP_FWD, 1>(const float*, float*, int, int, int,
+                                      int, int, const double*, const double*,
+                                      int, int, int, double, float*,
+                                      const float*, const float*,
+                                      const float*, cudaStream_t);
+template int launch_staged<OP_FWD, 2>(const float*, float*, int, int, int,
+                                      int, int, const double*, const double*,
+                                      int, int, int, double, float*,
+                                      const float*, const float*,
+                                      const float*, cudaStream_t);
+template int launch_staged<OP_BWD, 0>(const float*, float*, int, int, int,
+                                      int, int, const double*, const double*,
+                                      int, int, int, double, float*,
+                                      const float*, const float*,
+                                      const float*, cudaStream_t);
+
+}  // namespace cs

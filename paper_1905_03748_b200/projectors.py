@@ -107,9 +107,21 @@ def to_device(data, stream=None) -> torch.Tensor:
     return host.to(_device(), non_blocking=False)
 
 
+_PINNED_MIN_BYTES = 1 << 20
+
+
 def to_host(t) -> np.ndarray:
+    """Host numpy copy of a tensor.  Large device results drain through a
+    page-locked buffer (torch's caching host allocator) at full PCIe rate;
+    the returned array is a view that keeps that buffer alive."""
     if isinstance(t, torch.Tensor):
-        return t.detach().cpu().numpy()
+        t = t.detach()
+        if t.is_cuda and t.numel() * t.element_size() >= _PINNED_MIN_BYTES:
+            out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            out.copy_(t, non_blocking=True)
+            torch.cuda.current_stream(t.device).synchronize()
+            return out.numpy()
+        return t.cpu().numpy()
     return np.asarray(t)
 
 
@@ -327,10 +339,14 @@ def backproject_slab(projections: ProjectionStack, geometry: ScanGeometry,
     if not (0 <= a0 < a1 <= geometry.n_angles):
         raise ValueError(f"angle range {projections.angle_range} outside scan")
     if accumulate_into is None:
-        accumulate_into = Volume.zeros(
-            grid, slab_range,
-            device=_device() if projections.on_device else None)
-    elif accumulate_into.slab_range != (z0, z1):
+        # fresh accumulator: zeros on the device; host callers get host data
+        target = torch.zeros((z1 - z0, grid.n_y, grid.n_x),
+                             dtype=torch.float32, device=_device())
+        backproject_chunk_into(target, projections, geometry, (z0, z1), mode,
+                               tiles)
+        return Volume(grid, target if projections.on_device
+                      else to_host(target), (z0, z1))
+    if accumulate_into.slab_range != (z0, z1):
         raise ValueError("accumulate_into does not cover the slab range")
     # device accumulators are added to in place; host ones round-trip
     target = to_device(accumulate_into.data)

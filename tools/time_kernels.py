@@ -19,10 +19,13 @@ vol = cs.phantom(cs.PhantomKind.SHEPP_LOGAN_3D, g.voxel_grid, device=dev).data
 y = torch.empty((A, n, n), device=dev)
 K.fwd_interp(vol, g, (0, A), (0, n), y)
 acc = torch.zeros((n, n, n), device=dev)
+dense = torch.randn((A, n, n), device=dev, generator=torch.Generator(
+    device=dev).manual_seed(1))
 ops = {
     "fwd": lambda: K.fwd_interp(vol, g, (0, A), (0, n), y),
     "matched": lambda: K.bwd_matched(y, g, (0, A), (0, n), acc),
     "fdk": lambda: K.bwd_fdk(y, g, (0, A), (0, n), acc),
+    "matched_dense": lambda: K.bwd_matched(dense, g, (0, A), (0, n), acc),
 }
 out = {}
 for name, fn in ops.items():
