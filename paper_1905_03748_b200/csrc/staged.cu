@@ -35,31 +35,6 @@ __device__ __forceinline__ int qfloor(const March& m, int k, int axis) {
   return (int)floorf(fmaf((float)(k - (int)m.kc), m.B[axis], m.A[axis]));
 }
 
-// i -> (x, y, z) in a box [bz][by][bx] without integer division: float
-// reciprocal estimate + one correction step (i < 2^24).
-__device__ __forceinline__ void box_coords(int i, int bx, int bxy, float inv_bx,
-                                           float inv_bxy, int& x, int& y,
-                                           int& z) {
-  z = (int)((float)i * inv_bxy);
-  int rem = i - z * bxy;
-  if (rem < 0) {
-    z--;
-    rem += bxy;
-  } else if (rem >= bxy) {
-    z++;
-    rem -= bxy;
-  }
-  y = (int)((float)rem * inv_bx);
-  x = rem - y * bx;
-  if (x < 0) {
-    y--;
-    x += bx;
-  } else if (x >= bx) {
-    y++;
-    x -= bx;
-  }
-}
-
 // Red of a float4 quad (16-byte aligned) -- see backward.cu.
 __device__ __forceinline__ void st_red4(float* p, float a, float b, float c,
                                         float d) {
@@ -249,24 +224,33 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
       bn[0] = ((bo[0] + bn[0] - x0) + 3) & ~3;
       bo[0] = x0;
     }
-    const int bxy = bn[0] * bn[1];
-    const int bsize = bxy * bn[2];
-    const float inv_bx = 1.f / (float)bn[0], inv_bxy = 1.f / (float)bxy;
+    // Shared layout: the transverse axis is innermost, so the 32 lanes of a
+    // warp (adjacent detector columns = adjacent T) hit distinct banks:
+    //   M = y: [z][y][x] (x = T, unit stride; x-quads contiguous)
+    //   M = x: [z][x][y] (y = T, unit stride; odd x pitch -> no conflicts)
+    const int sx = M == 1 ? 1 : (bn[1] | 1);
+    const int sy = M == 1 ? bn[0] : 1;
+    const int sz = M == 1 ? bn[0] * bn[1] : bn[0] * sx;
+    const int bsize = sz * bn[2];
     const bool fits = !mixed && bsize <= box_cap;
+    const int qpr = bn[0] >> 2;            // x-quads per (y, z) row
+    const int nquads = qpr * bn[1] * bn[2];
+    const float inv_q = 1.f / (float)qpr, inv_y = 1.f / (float)bn[1];
+    // quad qi -> (x0 = 4 xq, y, z) box coordinates
+    auto quad_coords = [&](int qi, int& xq, int& by, int& bz) {
+      int row = (int)((float)qi * inv_q);
+      xq = qi - row * qpr;
+      if (xq < 0) { row--; xq += qpr; } else if (xq >= qpr) { row++; xq -= qpr; }
+      bz = (int)((float)row * inv_y);
+      by = row - bz * bn[1];
+      if (by < 0) { bz--; by += bn[1]; } else if (by >= bn[1]) { bz++; by -= bn[1]; }
+    };
 
     if (fits) {
       if (OP == OP_FWD) {
-        // one aligned float4 per thread and step: rows of bn[0] / 4 quads
-        const int qpr = bn[0] >> 2;
-        const int nquads = qpr * bn[1] * bn[2];
-        const float inv_q = 1.f / (float)qpr, inv_y = 1.f / (float)bn[1];
         for (int qi = threadIdx.x; qi < nquads; qi += ST_THREADS) {
-          int row = (int)((float)qi * inv_q);
-          int xq = qi - row * qpr;
-          if (xq < 0) { row--; xq += qpr; } else if (xq >= qpr) { row++; xq -= qpr; }
-          int bz = (int)((float)row * inv_y);
-          int by = row - bz * bn[1];
-          if (by < 0) { bz--; by += bn[1]; } else if (by >= bn[1]) { bz++; by -= bn[1]; }
+          int xq, by, bz;
+          quad_coords(qi, xq, by, bz);
           const int gx = bo[0] + 4 * xq, gy = bo[1] + by, gz = bo[2] + bz;
           float4 q4 = make_float4(0.f, 0.f, 0.f, 0.f);
           if (gy >= 0 && gy < ny && gz >= z_lo && gz < z_hi) {
@@ -281,7 +265,15 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
               if (gx + 3 >= 0 && gx + 3 < nx) q4.w = __ldg(src + gx + 3);
             }
           }
-          *reinterpret_cast<float4*>(st_box + row * bn[0] + 4 * xq) = q4;
+          const int d = bz * sz + by * sy + 4 * xq * sx;
+          if (M == 1) {
+            *reinterpret_cast<float4*>(st_box + d) = q4;
+          } else {
+            st_box[d] = q4.x;
+            st_box[d + sx] = q4.y;
+            st_box[d + 2 * sx] = q4.z;
+            st_box[d + 3 * sx] = q4.w;
+          }
         }
       } else {
         for (int i = threadIdx.x; i < bsize; i += ST_THREADS) box_i[i] = 0;
@@ -299,14 +291,14 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
         const float wx = qx - fx, wy = qy - fy, wz = qz - fz;
         const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
         if (fits) {
-          const int b = ((iz - bo[2]) * bn[1] + (iy - bo[1])) * bn[0] +
-                        (ix - bo[0]);
+          const int b = (iz - bo[2]) * sz + (iy - bo[1]) * sy +
+                        (ix - bo[0]) * sx;
           if (OP == OP_FWD) {
-            const float s000 = st_box[b], s001 = st_box[b + 1];
-            const float s010 = st_box[b + bn[0]], s011 = st_box[b + bn[0] + 1];
-            const float s100 = st_box[b + bxy], s101 = st_box[b + bxy + 1];
-            const float s110 = st_box[b + bxy + bn[0]];
-            const float s111 = st_box[b + bxy + bn[0] + 1];
+            const float s000 = st_box[b], s001 = st_box[b + sx];
+            const float s010 = st_box[b + sy], s011 = st_box[b + sy + sx];
+            const float s100 = st_box[b + sz], s101 = st_box[b + sz + sx];
+            const float s110 = st_box[b + sz + sy];
+            const float s111 = st_box[b + sz + sy + sx];
             const float r00 = fmaf(wx, s001 - s000, s000);
             const float r01 = fmaf(wx, s011 - s010, s010);
             const float r10 = fmaf(wx, s101 - s100, s100);
@@ -319,13 +311,13 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
             const float y00 = z0 * (1.f - wy), y01 = z0 * wy;
             const float y10 = z1 * (1.f - wy), y11 = z1 * wy;
             atomicAdd(&box_i[b], __float2int_rn(y00 * (1.f - wx)));
-            atomicAdd(&box_i[b + 1], __float2int_rn(y00 * wx));
-            atomicAdd(&box_i[b + bn[0]], __float2int_rn(y01 * (1.f - wx)));
-            atomicAdd(&box_i[b + bn[0] + 1], __float2int_rn(y01 * wx));
-            atomicAdd(&box_i[b + bxy], __float2int_rn(y10 * (1.f - wx)));
-            atomicAdd(&box_i[b + bxy + 1], __float2int_rn(y10 * wx));
-            atomicAdd(&box_i[b + bxy + bn[0]], __float2int_rn(y11 * (1.f - wx)));
-            atomicAdd(&box_i[b + bxy + bn[0] + 1], __float2int_rn(y11 * wx));
+            atomicAdd(&box_i[b + sx], __float2int_rn(y00 * wx));
+            atomicAdd(&box_i[b + sy], __float2int_rn(y01 * (1.f - wx)));
+            atomicAdd(&box_i[b + sy + sx], __float2int_rn(y01 * wx));
+            atomicAdd(&box_i[b + sz], __float2int_rn(y10 * (1.f - wx)));
+            atomicAdd(&box_i[b + sz + sx], __float2int_rn(y10 * wx));
+            atomicAdd(&box_i[b + sz + sy], __float2int_rn(y11 * (1.f - wx)));
+            atomicAdd(&box_i[b + sz + sy + sx], __float2int_rn(y11 * wx));
           }
         } else {
           // overflow path: straight from / to global memory
@@ -359,14 +351,19 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
     if (OP == OP_BWD && fits) {
       __syncthreads();
       // flush the box: one 16-byte reduction per aligned x-quad
-      const int nq = bsize >> 2;
-      for (int qd = threadIdx.x; qd < nq; qd += ST_THREADS) {
-        const int i = qd << 2;
-        const int4 q = *reinterpret_cast<const int4*>(box_i + i);
+      for (int qi = threadIdx.x; qi < nquads; qi += ST_THREADS) {
+        int xq, by, bz;
+        quad_coords(qi, xq, by, bz);
+        const int d = bz * sz + by * sy + 4 * xq * sx;
+        int4 q;
+        if (M == 1) {
+          q = *reinterpret_cast<const int4*>(box_i + d);
+        } else {
+          q = make_int4(box_i[d], box_i[d + sx], box_i[d + 2 * sx],
+                        box_i[d + 3 * sx]);
+        }
         if ((q.x | q.y | q.z | q.w) == 0) continue;
-        int bx, by, bz;
-        box_coords(i, bn[0], bxy, inv_bx, inv_bxy, bx, by, bz);
-        const int gx = bo[0] + bx, gy = bo[1] + by, gz = bo[2] + bz;
+        const int gx = bo[0] + 4 * xq, gy = bo[1] + by, gz = bo[2] + bz;
         if (gy < 0 || gy >= ny || gz < z_lo || gz >= z_hi) continue;
         float* dst = vol_acc + (size_t)(gz - z_lo) * plane + (size_t)gy * nx;
         const float f0 = (float)q.x * inv_scale, f1 = (float)q.y * inv_scale;
