@@ -21,6 +21,8 @@
 // kernels (same fp64 ray set-up, same fp32 lattice q(k) = A + (k - kc) B),
 // so chunking changes only summation order.  Boxes that would not fit the
 // shared-memory budget are served from global memory for that chunk.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cs {
@@ -55,7 +57,8 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
   constexpr int T = 1 - M;
   extern __shared__ float st_box[];
   int* box_i = reinterpret_cast<int*>(st_box);
-  __shared__ int ext[8];  // mlo, mhi, tlo, thi, zlo, zhi, dir-flags
+  __shared__ int ext[8];   // mlo, mhi, -, -, -, -, dir flags
+  __shared__ int ext8[8];  // per chunk candidate: tlo, thi, zlo, zhi (x2)
   __shared__ float s_scale;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -167,58 +170,80 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
   }
   // samples are consumed in index order in both march directions: chunk c
   // takes the next run of samples whose M-cell lies in it
+  // Chunks of ST_S cells along M in march order; a chunk whose box would
+  // not fit the shared budget is retried at ST_S / 2 cells (both candidate
+  // extents are reduced in one pass), and only then served from global.
   int k = k0;
-  const int n_chunks = mixed ? 0 : (mhi - mlo) / ST_S + 1;
-  for (int c = 0; c < n_chunks; c++) {
-    // chunk = M-cells [c_lo, c_hi] in march order
-    const int c_lo = dir > 0 ? mlo + c * ST_S : mhi - c * ST_S - ST_S + 1;
-    const int c_hi = c_lo + ST_S - 1;
-    const int ka = k;
-    int kb = k;
+  int cur = dir > 0 ? mlo : mhi;  // next M-cell in march order
+  const bool run = !mixed;
+  while (run && (dir > 0 ? cur <= mhi : cur >= mlo)) {
+    // candidate chunks: S = ST_S (index 0) and ST_S / 2 (index 1)
+    int kbc[2] = {k, k};
     if (has) {
-      // last sample of the chunk: qM(k) crosses the chunk's far face at
-      // k* = kc + (face - A_M) / B_M; estimate, then settle on the exact
-      // fp32 cell test (the same floor the sampling loop uses)
-      const float face = dir > 0 ? (float)(c_hi + 1) : (float)c_lo;
-      const float kst = (face - m.A[M]) / m.B[M] + (float)(int)m.kc;
-      int ke = (int)fminf(fmaxf(ceilf(kst), (float)k), (float)k1);
-      if (dir > 0) {
-        while (ke > k && qfloor(m, ke - 1, M) > c_hi) ke--;
-        while (ke < k1 && qfloor(m, ke, M) <= c_hi) ke++;
-      } else {
-        while (ke > k && qfloor(m, ke - 1, M) < c_lo) ke--;
-        while (ke < k1 && qfloor(m, ke, M) >= c_lo) ke++;
+#pragma unroll
+      for (int ci = 0; ci < 2; ci++) {
+        const int S = ST_S >> ci;
+        const int c_lo = dir > 0 ? cur : cur - S + 1;
+        const int c_hi = c_lo + S - 1;
+        // last sample of the chunk: qM(k) crosses the far face at
+        // k* = kc + (face - A_M) / B_M; estimate, then settle on the exact
+        // fp32 cell test (the same floor the sampling loop uses)
+        const float face = dir > 0 ? (float)(c_hi + 1) : (float)c_lo;
+        const float kst = (face - m.A[M]) / m.B[M] + (float)(int)m.kc;
+        int ke = (int)fminf(fmaxf(ceilf(kst), (float)k), (float)k1);
+        if (dir > 0) {
+          while (ke > k && qfloor(m, ke - 1, M) > c_hi) ke--;
+          while (ke < k1 && qfloor(m, ke, M) <= c_hi) ke++;
+        } else {
+          while (ke > k && qfloor(m, ke - 1, M) < c_lo) ke--;
+          while (ke < k1 && qfloor(m, ke, M) >= c_lo) ke++;
+        }
+        kbc[ci] = ke;
       }
-      kb = ke;
-      k = kb;
     }
-    const bool any = kb > ka;
     __syncthreads();  // previous chunk's box fully consumed
-    if (threadIdx.x == 0) {
-      ext[2] = INT_MAX;
-      ext[3] = INT_MIN;
-      ext[4] = INT_MAX;
-      ext[5] = INT_MIN;
+    if (threadIdx.x < 8) ext8[threadIdx.x] = (threadIdx.x & 1) ? INT_MIN : INT_MAX;
+    __syncthreads();
+#pragma unroll
+    for (int ci = 0; ci < 2; ci++) {
+      if (kbc[ci] > k) {
+        const int t0 = qfloor(m, k, T), t1 = qfloor(m, kbc[ci] - 1, T);
+        const int zz0 = qfloor(m, k, 2), zz1 = qfloor(m, kbc[ci] - 1, 2);
+        atomicMin(&ext8[4 * ci + 0], min(t0, t1));
+        atomicMax(&ext8[4 * ci + 1], max(t0, t1));
+        atomicMin(&ext8[4 * ci + 2], min(zz0, zz1));
+        atomicMax(&ext8[4 * ci + 3], max(zz0, zz1));
+      }
     }
     __syncthreads();
-    if (any) {
-      const int t0 = qfloor(m, ka, T), t1 = qfloor(m, kb - 1, T);
-      const int zz0 = qfloor(m, ka, 2), zz1 = qfloor(m, kb - 1, 2);
-      atomicMin(&ext[2], min(t0, t1));
-      atomicMax(&ext[3], max(t0, t1));
-      atomicMin(&ext[4], min(zz0, zz1));
-      atomicMax(&ext[5], max(zz0, zz1));
-    }
-    __syncthreads();
-    if (ext[2] > ext[3] && !mixed) continue;  // nobody samples this chunk
+    // box size for a candidate (same formula as the layout below)
+    auto box_size = [&](int ci, int S) {
+      const int c_lo = dir > 0 ? cur : cur - S + 1;
+      const int nt = ext8[4 * ci + 1] - ext8[4 * ci] + 2;
+      const int nzz = ext8[4 * ci + 3] - ext8[4 * ci + 2] + 2;
+      const int xlo = M == 0 ? c_lo : ext8[4 * ci];
+      const int xn = M == 0 ? S + 1 : nt;
+      const int nbx = ((xlo + xn - (xlo & ~3)) + 3) & ~3;
+      const int nby = M == 0 ? nt : S + 1;
+      return M == 1 ? nbx * nby * nzz : nbx * (nby | 1) * nzz;
+    };
+    const int ci = (ext8[0] > ext8[1] || box_size(0, ST_S) <= box_cap) ? 0 : 1;
+    const int S = ST_S >> ci;
+    const int c_lo = dir > 0 ? cur : cur - S + 1;
+    cur += dir * S;
+    const int ka = k;
+    const int kb = kbc[ci];
+    k = kb;
+    const bool any = kb > ka;
+    if (ext8[4 * ci] > ext8[4 * ci + 1]) continue;  // nobody samples it
     // box over taps: cells [lo, hi + 1] per axis; x padded to aligned quads
     int bo[3], bn[3];
     bo[M] = c_lo;
-    bn[M] = ST_S + 1;
-    bo[T] = ext[2];
-    bn[T] = ext[3] - ext[2] + 2;
-    bo[2] = ext[4];
-    bn[2] = ext[5] - ext[4] + 2;
+    bn[M] = S + 1;
+    bo[T] = ext8[4 * ci];
+    bn[T] = ext8[4 * ci + 1] - ext8[4 * ci] + 2;
+    bo[2] = ext8[4 * ci + 2];
+    bn[2] = ext8[4 * ci + 3] - ext8[4 * ci + 2] + 2;
     {
       const int x0 = bo[0] & ~3;
       bn[0] = ((bo[0] + bn[0] - x0) + 3) & ~3;
@@ -486,7 +511,8 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     release_geometry(dgeom, s);
     CS_CHECK_CUDA(e);
   }
-  const size_t smem = 64 * 1024;  // 3 CTAs per SM
+  static const char* kb_knob = getenv("CS_STAGED_SMEM_KB");
+  const size_t smem = (kb_knob ? (size_t)atoi(kb_knob) : 64) * 1024;
   const int cap = (int)(smem / sizeof(float));
   const float budget =
       OP == OP_BWD ? fixed_point_budget(grid6, nx, ny, nz, geom, n_a, n_u, n_v,
@@ -500,9 +526,9 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   static bool attr_set = false;  // per process; one device per ordinal
   if (!attr_set) {
     cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+                         200 * 1024);
     cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+                         200 * 1024);
     attr_set = true;
   }
   if (nxm > 0)
