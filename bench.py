@@ -233,9 +233,17 @@ def run_ours(args):
     from paper_1905_03748_b200 import kernels as K
 
     rank, world, local = env_rank()
+    # one rank per GPU; CS_BENCH_BACKEND=gloo lets several ranks share a GPU
+    # to exercise the N>1 path on a 1-GPU box (timings then are not scaling)
+    backend = os.environ.get("CS_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl",
+                                    device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     n, A1 = args.size, args.angles
     A = A1 * world
     g = make_geometry(n, A, cs)
@@ -294,7 +302,8 @@ def run_ours(args):
     t_ax = sum(e[0].elapsed_time(e[1]) for e in ev) * 1e-3 / args.steps
     t_atb = sum(e[1].elapsed_time(e[2]) for e in ev) * 1e-3 / args.steps
     if world > 1:
-        t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+        t = torch.tensor([elapsed], dtype=torch.float64,
+                         device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
     upd_ax = float(A1) * n ** 3

@@ -319,3 +319,30 @@ def test_tigre_aliases():
     assert rel_l2(v, O.bwd_fdk(p, to_oracle(g))) <= TOL_OP
     r = cs.sirt(p, g, niter=2)
     assert r.shape == (16, 16, 16)
+
+
+def test_out_of_core_loops_match_in_core():
+    """A device budget too small for the volume forces slab streaming
+    (plan.n_splits > 1); CGLS / OS-SART through the out-of-core executor
+    must match the in-core device loops."""
+    n, na = 24, 12
+    g = synth_geometry(n, na)
+    x = cs.phantom(cs.PhantomKind.SHEPP_LOGAN_3D, g.voxel_grid).data
+    b = cs.forward_project_slab(cs.Volume(g.voxel_grid, x), g, (0, na), IP)
+    big = cs.DevicePool((cs.DeviceSpec(memory_budget=2 ** 30),))
+    small = cs.DevicePool((cs.DeviceSpec(memory_budget=98000),))
+    assert cs.plan_forward(g, small).n_splits > 1
+    assert cs.plan_backward(g, small).n_splits > 1
+    r_in = cs.cgls(b, g, cs.ReconConfig(big, iterations=3))
+    sink = []
+    r_out = cs.cgls(b, g, cs.ReconConfig(small, iterations=3), trace_sink=sink)
+    assert rel_l2(r_out.volume.data, r_in.volume.data) <= TOL_LOOP
+    np.testing.assert_allclose(r_out.residuals, r_in.residuals, rtol=TOL_LOOP)
+    assert sink and all(max(t.high_water.values()) <= 98000 for t in sink)
+    for t in sink:
+        cs.check_trace(t, small)
+    cfg_in = cs.ReconConfig(big, cs.Algorithm.OSSART, 2, 4)
+    cfg_out = cs.ReconConfig(small, cs.Algorithm.OSSART, 2, 4)
+    o_in = cs.os_sart(b, g, cfg_in).data
+    o_out = cs.os_sart(b, g, cfg_out).data
+    assert rel_l2(o_out, o_in) <= TOL_LOOP
