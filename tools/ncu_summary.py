@@ -30,6 +30,7 @@ METRICS = [
     ("smsp__inst_executed.sum", "warp insts"),
 ]
 KEYS = {"fwd_interp": "fwd_interp_kernel", "bwd_matched": "bwd_matched_kernel",
+        "staged_kernel<1": "bwd_matched_kernel",
         "bwd_fdk": "bwd_fdk_kernel", "fwd_siddon": "fwd_siddon_kernel"}
 
 
@@ -47,6 +48,7 @@ def main():
         traffic = json.load(open(traffic_path))
     except (OSError, ValueError):
         traffic = {}
+    sums = {}
     for rep in reps:
         txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
                              capture_output=True, text=True).stdout
@@ -68,7 +70,10 @@ def main():
                     except ValueError:
                         continue
                     if rd == rd and wr == wr:  # skip failed (nan) captures
-                        traffic[key] = rd + wr
+                        # one C-ABI call may be several kernels (staged
+                        # matched = x-major + y-major views): sum them
+                        sums[key] = sums.get(key, 0.0) + rd + wr
+    traffic.update(sums)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     md = [f"# ncu --set full summary ({tag})", "",
           "Captured with `ncu --set full --clock-control none --import-source on`"

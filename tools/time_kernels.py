@@ -27,6 +27,22 @@ ops = {
     "fdk": lambda: K.bwd_fdk(y, g, (0, A), (0, n), acc),
     "matched_dense": lambda: K.bwd_matched(dense, g, (0, A), (0, n), acc),
 }
+u2 = torch.empty_like(vol)
+ss = torch.zeros(1, dtype=torch.float64, device=dev)
+p3 = torch.zeros((3, n, n, n), device=dev)
+q3 = torch.empty_like(p3)
+
+
+def tv_gd():
+    K.tv_grad_sumsq(vol, (0, n), ss)
+    K.tv_step(vol, u2, 1e-3, ss, 1.0)
+
+
+ops["tv_gd_iter"] = tv_gd
+ops["rof_iter"] = lambda: K.rof_iter(vol, p3, q3, 0.1)
+only = os.environ.get("PROF_ONLY")
+if only:
+    ops = {k: v for k, v in ops.items() if k in only.split(",")}
 out = {}
 for name, fn in ops.items():
     fn()
@@ -38,5 +54,10 @@ for name, fn in ops.items():
     e.record()
     torch.cuda.synchronize()
     t = s.elapsed_time(e) / R * 1e-3
-    out[name] = {"ms": t * 1e3, "gups": A * n ** 3 / t / 1e9}
+    if name in ("tv_gd_iter", "rof_iter"):
+        bpv = 12.0 if name == "tv_gd_iter" else 28.0
+        out[name] = {"ms": t * 1e3, "gvox_per_s": n ** 3 / t / 1e9,
+                     "frac_hbm": n ** 3 * bpv / t / 6550.7e9}
+    else:
+        out[name] = {"ms": t * 1e3, "gups": A * n ** 3 / t / 1e9}
 print(json.dumps({"tag": os.environ.get("TAG", ""), **out}))
