@@ -31,7 +31,8 @@ METRICS = [
 ]
 KEYS = {"fwd_interp": "fwd_interp_kernel", "bwd_matched": "bwd_matched_kernel",
         "staged_kernel<1": "bwd_matched_kernel",
-        "bwd_fdk": "bwd_fdk_kernel", "fwd_siddon": "fwd_siddon_kernel"}
+        "bwd_fdk": "bwd_fdk_kernel", "fdk_staged": "bwd_fdk_kernel",
+        "fwd_siddon": "fwd_siddon_kernel"}
 
 
 def to_bytes(v, unit):

@@ -26,6 +26,7 @@ ops = {
     "matched": lambda: K.bwd_matched(y, g, (0, A), (0, n), acc),
     "fdk": lambda: K.bwd_fdk(y, g, (0, A), (0, n), acc),
     "matched_dense": lambda: K.bwd_matched(dense, g, (0, A), (0, n), acc),
+    "siddon": lambda: K.fwd_siddon(vol, g, (0, A), (0, n), y),
 }
 u2 = torch.empty_like(vol)
 ss = torch.zeros(1, dtype=torch.float64, device=dev)
