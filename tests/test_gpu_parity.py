@@ -346,3 +346,83 @@ def test_out_of_core_loops_match_in_core():
     o_in = cs.os_sart(b, g, cfg_in).data
     o_out = cs.os_sart(b, g, cfg_out).data
     assert rel_l2(o_out, o_in) <= TOL_LOOP
+
+
+def _odd_geometry(nx, ny, nz, nu, nv, na, voxel=(1.0, 0.9, 1.1),
+                  offset=(0.3, -0.2, 0.1), pitch=None, det_off=(0.4, -0.3)):
+    grid = cs.VoxelGrid(nx, ny, nz, voxel, offset)
+    r = grid.bounding_radius()
+    dso, dsd = 2.5 * r + 2.0, 5.0 * r + 4.0
+    if pitch is None:
+        ext = grid.extent
+        mag = dsd / dso
+        pitch = (1.3 * mag * max(ext[0], ext[1]) / nu,
+                 1.3 * mag * ext[2] / nv)
+    det = cs.DetectorGrid(nu, nv, pitch, det_off)
+    angles = tuple(np.linspace(0.1, 0.1 + 2 * math.pi, na, endpoint=False))
+    return cs.ScanGeometry(dso, dsd, angles, grid, det)
+
+
+@pytest.mark.parametrize("shape", [(13, 11, 9, 17, 15, 7), (30, 26, 21, 33, 19, 11)])
+def test_odd_sizes_vs_oracle(shape):
+    """Sizes that are not multiples of 4 (scalar flush / load paths of the
+    staged kernels), anisotropic voxels, offsets, slabs and windows."""
+    nx, ny, nz, nu, nv, na = shape
+    g = _odd_geometry(nx, ny, nz, nu, nv, na)
+    og = to_oracle(g)
+    rng = np.random.default_rng(11)
+    x = rng.random((nz, ny, nx), dtype=np.float32)
+    y = rng.standard_normal((na, nv, nu)).astype(np.float32)
+    z0, z1 = nz // 3, nz - 2
+    a0, a1 = 1, na - 1
+    for (zr, ar) in (((0, nz), (0, na)), ((z0, z1), (a0, a1))):
+        xs = x[zr[0]:zr[1]]
+        got = cs.forward_project_slab(cs.Volume(g.voxel_grid, xs, zr), g, ar,
+                                      IP).data
+        assert rel_l2(got, O.fwd_interp(xs, og, ar, zr)) <= TOL_OP
+        ys = y[ar[0]:ar[1]]
+        st = cs.ProjectionStack(g.detector, ys, ar)
+        for mode, ofn in ((cs.WeightMode.MATCHED, O.bwd_matched),
+                          (cs.WeightMode.FDK, O.bwd_fdk)):
+            got = cs.backproject_slab(st, g, zr, mode).data
+            assert rel_l2(got, ofn(ys, og, ar, zr)) <= TOL_OP, mode
+
+
+def test_fdk_oversized_footprint_direct_path():
+    """Detector pixels much finer than voxels: a CTA's per-view footprint
+    exceeds the shared staging buffer and the view is gathered directly."""
+    g = _odd_geometry(16, 16, 16, 420, 400, 2, voxel=(1.0, 1.0, 1.0),
+                      offset=(0.0, 0.0, 0.0), pitch=(0.1, 0.1),
+                      det_off=(0.0, 0.0))
+    og = to_oracle(g)
+    y = np.random.default_rng(2).standard_normal((2, 400, 420)).astype(
+        np.float32)
+    got = cs.backproject_slab(cs.ProjectionStack(g.detector, y), g, (0, 16),
+                              cs.WeightMode.FDK).data
+    assert rel_l2(got, O.bwd_fdk(y, og)) <= TOL_OP
+
+
+def test_staged_small_box_budget_subprocess():
+    """With a tiny shared-memory box budget the staged matched kernel halves
+    its chunk depth and then falls back to global reductions; results must
+    not change (runs in a subprocess: the budget knob is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path[:0] = [%r, %r]\n"
+        "import numpy as np, paper_1905_03748_b200 as cs\n"
+        "from conftest import synth_geometry, to_oracle, rel_l2\n"
+        "from oracle import oracle as O\n"
+        "g = synth_geometry(40, 12)\n"
+        "y = np.random.default_rng(4).standard_normal((12, 40, 40)).astype(np.float32)\n"
+        "got = cs.backproject_slab(cs.ProjectionStack(g.detector, y), g, (0, 40), cs.WeightMode.MATCHED).data\n"
+        "e = rel_l2(got, O.bwd_matched(y, to_oracle(g)))\n"
+        "print(e); assert e <= 1e-5\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+         os.path.dirname(os.path.abspath(__file__)))
+    for kb in ("2", "6"):
+        env = dict(os.environ, CS_STAGED_SMEM_KB=kb)
+        r = subprocess.run([sys.executable, "-c", code], env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
