@@ -242,6 +242,19 @@ void release_geometry(AngleGeom* d_geom, cudaStream_t s);
 
 Grid make_grid(const double grid6[6], int nx, int ny, int nz);
 
+// Detector rows [v0, v1) whose rays can touch slices [z_lo, z_hi) in any of
+// the n_a views (full range for a full-height slab); runtime.cu.
+void slab_row_band(const double* geom, int n_a, const Grid& G, int z_lo,
+                   int z_hi, int n_v, int* v0, int* v1);
+
+// Knob: CS_NO_CULL=1 disables v-band culling (A/B runs).
+bool cull_enabled();
+
+// Zero rows [0, v0) and [v1, n_v) of every view of out[n_a][n_v][n_u]
+// (the overwrite-mode result of the culled rows).
+int zero_rows_outside(float* out, int n_a, int n_u, int n_v, int v0, int v1,
+                      cudaStream_t s);
+
 // Shared-memory staged Ax / matched Atb (staged.cu).
 enum StOpKind { OP_FWD = 0, OP_BWD = 1 };
 template <int OP, int MODE>

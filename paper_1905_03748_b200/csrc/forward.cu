@@ -25,10 +25,12 @@ enum FwdMode { FWD_OVERWRITE = 0, FWD_ACCUMULATE = 1, FWD_RESIDUAL = 2 };
 constexpr int FWD_TILE_U = 16;  // per CTA
 constexpr int FWD_TILE_V = 8;
 
-__device__ __forceinline__ void tile_coords(int& u, int& v) {
+// v_base: first detector row of the launch (v-band culling: rows whose rays
+// cannot reach the slab are not launched, runtime.cu slab_row_band).
+__device__ __forceinline__ void tile_coords(int& u, int& v, int v_base) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   u = blockIdx.x * FWD_TILE_U + (warp & 1) * 8 + (lane & 7);
-  v = blockIdx.y * FWD_TILE_V + (warp >> 1) * 4 + (lane >> 3);
+  v = v_base + blockIdx.y * FWD_TILE_V + (warp >> 1) * 4 + (lane >> 3);
 }
 
 template <int MODE>
@@ -36,12 +38,13 @@ __global__ void __launch_bounds__(128)
     fwd_interp_kernel(cudaTextureObject_t tex,
                       const AngleGeom* __restrict__ geom, Grid G,
                       double step_max, int z_lo, int z_hi, int n_u, int n_v,
-                      float* __restrict__ out, const float* __restrict__ b,
+                      int v_base, int v_end, float* __restrict__ out,
+                      const float* __restrict__ b,
                       const float* __restrict__ w) {
   int u, v;
-  tile_coords(u, v);
+  tile_coords(u, v, v_base);
   const int a = blockIdx.z;
-  if (u >= n_u || v >= n_v) return;
+  if (u >= n_u || v >= v_end) return;
   Ray r;
   setup_ray(geom[a], G, step_max, u, v, r);
   float acc = 0.f;
@@ -101,12 +104,12 @@ __global__ void __launch_bounds__(128)
 __global__ void __launch_bounds__(128)
     fwd_siddon_kernel(const float* __restrict__ vol,
                       const AngleGeom* __restrict__ geom, Grid G, int z_lo,
-                      int z_hi, int n_u, int n_v, float* __restrict__ out,
-                      int accumulate) {
+                      int z_hi, int n_u, int n_v, int v_base, int v_end,
+                      float* __restrict__ out, int accumulate) {
   int u, v;
-  tile_coords(u, v);
+  tile_coords(u, v, v_base);
   const int a = blockIdx.z;
-  if (u >= n_u || v >= n_v) return;
+  if (u >= n_u || v >= v_end) return;
   const AngleGeom g = geom[a];
   double o[3] = {g.src[0], g.src[1], g.src[2]}, d[3];
   pixel_direction(g, u, v, d);
@@ -202,22 +205,31 @@ static int launch_interp(const float* vol, int nx, int ny, int nz, int z_lo,
   // Slabs taller than the layer limit go through in sub-slabs;
   // the first sub-slab applies MODE, the rest accumulate.
   const dim3 block(128);
-  const dim3 grid((n_u + FWD_TILE_U - 1) / FWD_TILE_U,
-                  (n_v + FWD_TILE_V - 1) / FWD_TILE_V, n_a);
   const size_t plane = (size_t)nx * ny;
   for (int s0 = z_lo; s0 < z_hi; s0 += maxl) {
     const int s1 = min(z_hi, s0 + maxl);
+    const bool first = s0 == z_lo;
+    int v0 = 0, v1 = n_v;
+    if (MODE != FWD_RESIDUAL && cull_enabled())
+      slab_row_band(geom, n_a, G, s0, s1, n_v, &v0, &v1);
+    if (first && MODE == FWD_OVERWRITE &&
+        (rc = zero_rows_outside(out, n_a, n_u, n_v, v0, v1, s))) {
+      release_geometry(dgeom, s);
+      return rc;
+    }
+    if (v1 <= v0) continue;
+    const dim3 grid((n_u + FWD_TILE_U - 1) / FWD_TILE_U,
+                    (v1 - v0 + FWD_TILE_V - 1) / FWD_TILE_V, n_a);
     LayeredTexture* t = nullptr;
     if ((rc = load_layered(TEX_VOLUME, vol + (size_t)(s0 - z_lo) * plane, nx,
                            ny, s1 - s0, s, &t))) {
       release_geometry(dgeom, s);
       return rc;
     }
-    const bool first = s0 == z_lo;
     auto kern = first ? fwd_interp_kernel<MODE>
                       : fwd_interp_kernel<FWD_ACCUMULATE>;
     kern<<<grid, block, 0, s>>>(t->tex, dgeom, G, step_max, s0, s1, n_u, n_v,
-                                out, first ? b : nullptr,
+                                v0, v1, out, first ? b : nullptr,
                                 first ? w : nullptr);
     CS_CHECK_CUDA(cudaGetLastError());
   }
@@ -268,11 +280,20 @@ int cs_fwd_siddon(const float* vol, int nx, int ny, int nz, int z_lo,
   const Grid G = make_grid(grid6, nx, ny, nz);
   AngleGeom* dgeom = nullptr;
   if ((rc = upload_geometry(geom, n_a, s, &dgeom))) return rc;
-  const dim3 grid((n_u + FWD_TILE_U - 1) / FWD_TILE_U,
-                  (n_v + FWD_TILE_V - 1) / FWD_TILE_V, n_a);
-  fwd_siddon_kernel<<<grid, 128, 0, s>>>(vol, dgeom, G, z_lo, z_hi, n_u, n_v,
-                                         out, accumulate);
-  cudaError_t e = cudaGetLastError();
+  int v0 = 0, v1 = n_v;
+  if (cull_enabled()) slab_row_band(geom, n_a, G, z_lo, z_hi, n_v, &v0, &v1);
+  if (!accumulate && (rc = zero_rows_outside(out, n_a, n_u, n_v, v0, v1, s))) {
+    release_geometry(dgeom, s);
+    return rc;
+  }
+  cudaError_t e = cudaSuccess;
+  if (v1 > v0) {
+    const dim3 grid((n_u + FWD_TILE_U - 1) / FWD_TILE_U,
+                    (v1 - v0 + FWD_TILE_V - 1) / FWD_TILE_V, n_a);
+    fwd_siddon_kernel<<<grid, 128, 0, s>>>(vol, dgeom, G, z_lo, z_hi, n_u,
+                                           n_v, v0, v1, out, accumulate);
+    e = cudaGetLastError();
+  }
   release_geometry(dgeom, s);
   CS_CHECK_CUDA(e);
   return CS_OK;

@@ -1,6 +1,7 @@
 // runtime.cu -- error state, texture cache and geometry upload for the
 // conesplit B200 C-ABI.
 #include <cstdarg>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -135,6 +136,79 @@ int upload_geometry(const double* geom, int n_a, cudaStream_t s,
 
 void release_geometry(AngleGeom* d_geom, cudaStream_t s) {
   if (d_geom) cudaFreeAsync(d_geom, s);
+}
+
+bool cull_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* k = getenv("CS_NO_CULL");
+    on = (k && k[0] == '1') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+int zero_rows_outside(float* out, int n_a, int n_u, int n_v, int v0, int v1,
+                      cudaStream_t s) {
+  const size_t row = (size_t)n_u * sizeof(float);
+  const size_t pitch = row * n_v;
+  if (v1 <= v0) {
+    CS_CHECK_CUDA(cudaMemsetAsync(out, 0, pitch * n_a, s));
+    return CS_OK;
+  }
+  if (v0 > 0)
+    CS_CHECK_CUDA(cudaMemset2DAsync(out, pitch, 0, row * v0, n_a, s));
+  if (v1 < n_v)
+    CS_CHECK_CUDA(cudaMemset2DAsync(out + (size_t)v1 * n_u, pitch, 0,
+                                    row * (n_v - v1), n_a, s));
+  return CS_OK;
+}
+
+// Detector-row band of a slab (v-band culling).  A sample
+// can put a trilinear tap on a slice of [z_lo, z_hi) only if its z lies in
+// (gz0 + (z_lo - 1/2) vz, gz0 + (z_hi + 1/2) vz); every sample lies in the
+// grid box.  The rays through that slab box hit the detector inside the
+// projective image of its 8 corners (a convex box in front of the source
+// maps to the convex hull of its corner images), so rows outside
+// [min v - 2, max v + 2] never touch the slab.  Margins: 1.5 voxels in z, 2
+// rows on the detector.  Returns the union over the n_a views.
+void slab_row_band(const double* geom, int n_a, const Grid& G, int z_lo,
+                   int z_hi, int n_v, int* v0, int* v1) {
+  *v0 = 0;
+  *v1 = n_v;
+  if (z_lo <= 0 && z_hi >= G.n[2]) return;
+  const double zlo = G.g0[2] + (z_lo - 1.5) * G.vox[2];
+  const double zhi = G.g0[2] + (z_hi + 1.5) * G.vox[2];
+  const double xlo = G.g0[0] - G.vox[0], xhi = G.g0[0] + (G.n[0] + 1) * G.vox[0];
+  const double ylo = G.g0[1] - G.vox[1], yhi = G.g0[1] + (G.n[1] + 1) * G.vox[1];
+  double bmin = 1e300, bmax = -1e300;
+  for (int a = 0; a < n_a; a++) {
+    const double* g = geom + 12 * a;
+    const double *S = g, *D = g + 3, *us = g + 6, *vs = g + 9;
+    const double nrm[3] = {us[1] * vs[2] - us[2] * vs[1],
+                           us[2] * vs[0] - us[0] * vs[2],
+                           us[0] * vs[1] - us[1] * vs[0]};
+    const double vv = vs[0] * vs[0] + vs[1] * vs[1] + vs[2] * vs[2];
+    const double num = nrm[0] * (D[0] - S[0]) + nrm[1] * (D[1] - S[1]) +
+                       nrm[2] * (D[2] - S[2]);
+    for (int c = 0; c < 8; c++) {
+      const double P[3] = {(c & 1) ? xhi : xlo, (c & 2) ? yhi : ylo,
+                           (c & 4) ? zhi : zlo};
+      const double d[3] = {P[0] - S[0], P[1] - S[1], P[2] - S[2]};
+      const double den = nrm[0] * d[0] + nrm[1] * d[1] + nrm[2] * d[2];
+      const double t = num / den;
+      if (!(den * num > 0.0) || !(t > 0.0)) return;  // corner not in front
+      double b = 0.0;
+      for (int i = 0; i < 3; i++) b += (S[i] + t * d[i] - D[i]) * vs[i];
+      b /= vv;
+      bmin = fmin(bmin, b);
+      bmax = fmax(bmax, b);
+    }
+  }
+  if (!(bmin <= bmax)) return;
+  const double lo = floor(bmin) - 2.0, hi = ceil(bmax) + 3.0;
+  *v0 = lo <= 0.0 ? 0 : (lo >= n_v ? n_v : (int)lo);
+  *v1 = hi >= n_v ? n_v : (hi <= 0.0 ? 0 : (int)hi);
+  if (*v1 < *v0) *v1 = *v0;
 }
 
 }  // namespace cs

@@ -22,6 +22,7 @@
 // so chunking changes only summation order.  Boxes that would not fit the
 // shared-memory budget are served from global memory for that chunk.
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -50,7 +51,7 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
     staged_kernel(const float* __restrict__ vol_in, float* __restrict__ vol_acc,
                   const AngleGeom* __restrict__ geom,
                   const int* __restrict__ view_ids, Grid G, double step_max,
-                  int z_lo, int z_hi, int n_u, int n_v,
+                  int z_lo, int z_hi, int n_u, int n_v, int v_base, int v_end,
                   float* __restrict__ out, const float* __restrict__ proj_in,
                   const float* __restrict__ rb, const float* __restrict__ rw,
                   int box_cap, float fx_budget, int vec_ok) {
@@ -63,9 +64,9 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int u = blockIdx.x * ST_TU + lane;
-  const int v = blockIdx.y * ST_TV + warp;
+  const int v = v_base + blockIdx.y * ST_TV + warp;
   const int a = view_ids[blockIdx.z];
-  const bool valid = u < n_u && v < n_v;
+  const bool valid = u < n_u && v < v_end;
   const int nx = G.n[0], ny = G.n[1];
   const size_t plane = (size_t)nx * ny;
   const size_t pix = ((size_t)a * n_v + v) * n_u + u;
@@ -520,7 +521,53 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
                    : 0.f;
   const void* vbase = OP == OP_BWD ? (const void*)vol_acc : (const void*)vol_in;
   const int vec_ok = (nx % 4 == 0) && (((uintptr_t)vbase & 15) == 0);
-  const unsigned gx = (n_u + ST_TU - 1) / ST_TU, gy = (n_v + ST_TV - 1) / ST_TV;
+  // v-band culling per main-axis class (runtime.cu slab_row_band); the
+  // overwrite-mode Ax zeroes the culled rows
+  int band[2][2] = {{0, n_v}, {0, n_v}};
+  if (cull_enabled() && MODE != 2) {
+    double* gsub = (double*)malloc(sizeof(double) * 12 * (size_t)n_a);
+    for (int c = 0; c < 2; c++) {
+      const int lo = c == 0 ? 0 : nxm, hi = c == 0 ? nxm : nall;
+      ids_h = (int*)malloc(sizeof(int) * (size_t)n_a);
+      int m = 0;
+      for (int a = 0; a < n_a; a++)
+        if (view_axis(geom + 12 * a, n_u, n_v) == c) ids_h[m++] = a;
+      for (int i = 0; i < m; i++)
+        memcpy(gsub + 12 * i, geom + 12 * ids_h[i], 12 * sizeof(double));
+      free(ids_h);
+      if (hi > lo)
+        slab_row_band(gsub, hi - lo, G, z_lo, z_hi, n_v, &band[c][0],
+                      &band[c][1]);
+    }
+    free(gsub);
+    if (OP == OP_FWD && MODE == 0) {
+      // rows outside a class's band are zero for that class's views;
+      // zero outside the union (rows inside it are written by the kernels
+      // of both classes or lie in one class's band)
+      int v0 = n_v, v1 = 0;
+      for (int c = 0; c < 2; c++)
+        if ((c == 0 ? nxm : nall - nxm) > 0) {
+          v0 = min(v0, band[c][0]);
+          v1 = max(v1, band[c][1]);
+        }
+      if (v1 < v0) v0 = v1 = 0;
+      for (int c = 0; c < 2; c++) {
+        // launch rows as the union so every view's rows are written
+        band[c][0] = v0;
+        band[c][1] = v1;
+      }
+      rc = zero_rows_outside(out, n_a, n_u, n_v, v0, v1, s);
+      if (rc) {
+        cudaFreeAsync(ids, s);
+        release_geometry(dgeom, s);
+        return rc;
+      }
+    }
+  }
+  const unsigned gx = (n_u + ST_TU - 1) / ST_TU;
+  auto rows = [&](int c) {
+    return (unsigned)((band[c][1] - band[c][0] + ST_TV - 1) / ST_TV);
+  };
   auto k0 = staged_kernel<OP, 0, MODE>;
   auto k1 = staged_kernel<OP, 1, MODE>;
   static bool attr_set = false;  // per process; one device per ordinal
@@ -531,14 +578,14 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
                          200 * 1024);
     attr_set = true;
   }
-  if (nxm > 0)
-    k0<<<dim3(gx, gy, nxm), ST_THREADS, smem, s>>>(
-        vol_in, vol_acc, dgeom, ids, G, step_max, z_lo, z_hi, n_u, n_v, out,
-        proj_in, rb, rw, cap, budget, vec_ok);
-  if (nall > nxm)
-    k1<<<dim3(gx, gy, nall - nxm), ST_THREADS, smem, s>>>(
+  if (nxm > 0 && rows(0) > 0)
+    k0<<<dim3(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
+        vol_in, vol_acc, dgeom, ids, G, step_max, z_lo, z_hi, n_u, n_v,
+        band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_ok);
+  if (nall > nxm && rows(1) > 0)
+    k1<<<dim3(gx, rows(1), nall - nxm), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids + nxm, G, step_max, z_lo, z_hi, n_u, n_v,
-        out, proj_in, rb, rw, cap, budget, vec_ok);
+        band[1][0], band[1][1], out, proj_in, rb, rw, cap, budget, vec_ok);
   e = cudaGetLastError();
   cudaFreeAsync(ids, s);
   release_geometry(dgeom, s);

@@ -150,7 +150,10 @@ class _Pinned:
     """Page-lock a host numpy image for the pass (execution.py:117-124)."""
 
     def __init__(self, arr: np.ndarray | None, enabled: bool, events: list):
+        # file-backed images (fileio mmap) are streamed through pinned
+        # staging buffers instead: page-locking would read the whole file
         self.arr = arr if (enabled and isinstance(arr, np.ndarray)
+                           and not isinstance(arr, np.memmap)
                            and arr.nbytes > 0) else None
         self.events = events
         self.ok = False
@@ -177,6 +180,61 @@ class _Pinned:
                                           time.perf_counter() - t0,
                                           self.arr.nbytes))
         return False
+
+
+class _Staging:
+    """Pinned host ring for host sources that are not page-locked
+    (file-backed memmaps, or pinning disabled): each upload copies the
+    piece into a pinned buffer on the host (multi-threaded numpy copy, the
+    GIL is released) and enqueues the H2D from it, so slab s+1 is read from
+    the page cache while slab s computes.  A buffer is reused only after
+    its previous H2D completed."""
+
+    def __init__(self, nbuf: int, max_elems: int):
+        self.bufs = [torch.empty(max(1, max_elems), dtype=torch.float32,
+                                 pin_memory=True) for _ in range(nbuf)]
+        self.done = [None] * nbuf
+        self.next = 0
+
+    @staticmethod
+    def _copy(dst: np.ndarray, src: np.ndarray):
+        n = src.shape[0]
+        if src.nbytes < (64 << 20) or n < 2:
+            np.copyto(dst, src)
+            return
+        parts = min(8, n)
+        step = -(-n // parts)
+        ts = [threading.Thread(target=np.copyto,
+                               args=(dst[j:j + step], src[j:j + step]))
+              for j in range(0, n, step)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+
+    def upload(self, dst: torch.Tensor, src: np.ndarray, stream):
+        b = self.next % len(self.bufs)
+        self.next += 1
+        if self.done[b] is not None:
+            self.done[b].synchronize()
+        flat = self.bufs[b][:src.size]
+        self._copy(flat.numpy().reshape(src.shape), src)
+        with torch.cuda.stream(stream):
+            dst.copy_(flat.view(dst.shape), non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self.done[b] = ev
+
+
+def _upload(dst: torch.Tensor, src, stream, staging: "_Staging | None"):
+    """H2D (or D2D) of one slab / chunk on ``stream``."""
+    if isinstance(src, np.ndarray):
+        if staging is not None:
+            staging.upload(dst, src, stream)
+            return
+        src = torch.from_numpy(np.ascontiguousarray(src))
+    with torch.cuda.stream(stream):
+        dst.copy_(src, non_blocking=True)
 
 
 def _join_streams(dev: _Device):
@@ -281,7 +339,16 @@ def execute_forward(volume: Volume, geometry: ScanGeometry, pool: DevicePool,
                     tiles: ForwardTileSpec = ForwardTileSpec(),
                     trace_sink: list | None = None) -> ProjectionStack:
     """Run a planned forward pass (execution.py:175-246); equals the
-    monolithic projection of the full volume."""
+    monolithic projection of the full volume.
+
+    Per device: when its angle window fits beside two slab buffers, the
+    window stays resident as the accumulator (slab s+1 uploads while slab s
+    projects; later slabs accumulate in the kernel epilogue).  Otherwise the
+    window is processed in ``plan.chunk_angles`` chunks exactly as
+    Algorithm 1: per slab, per chunk, the partial projection is staged back
+    in (TransferIn), accumulated by the kernel and drained (TransferOut).
+    Host images that are not page-locked (file-backed memmaps) stream
+    through pinned staging buffers."""
     _validate(plan, OpKind.FORWARD, geometry, pool)
     grid, det = geometry.voxel_grid, geometry.detector
     if volume.slab_range != (0, grid.n_z):
@@ -295,6 +362,8 @@ def execute_forward(volume: Volume, geometry: ScanGeometry, pool: DevicePool,
     host_events: list = []
     fwd = K.fwd_interp if method is ProjectionMethod.INTERPOLATED \
         else K.fwd_siddon
+    pin = _Pinned(volume.data if not on_dev else None, plan.pin_host_image,
+                  host_events)
 
     def work(i: int):
         a0, a1 = plan.angle_assignment[i]
@@ -303,10 +372,10 @@ def execute_forward(volume: Volume, geometry: ScanGeometry, pool: DevicePool,
         dev = _Device(i, _cuda_device(pool, i), pool.devices[i].memory_budget)
         devs[i] = dev
         with torch.cuda.device(dev.cuda):
-            acc = dev.alloc((a1 - a0, det.n_v, det.n_u))
             src = volume.data
             if on_dev and src.device == dev.cuda and plan.n_splits == 1:
                 # device-resident input that fits: no staging
+                acc = dev.alloc((a1 - a0, det.n_v, det.n_u))
                 ev = dev.begin(dev.compute, "Kernel", "s0.c0")
                 with torch.cuda.stream(dev.compute):
                     dev.compute.wait_stream(torch.cuda.current_stream(
@@ -314,55 +383,143 @@ def execute_forward(volume: Volume, geometry: ScanGeometry, pool: DevicePool,
                     fwd(src, geometry, (a0, a1), (0, grid.n_z), acc,
                         False, dev.compute)
                 dev.end(ev, dev.compute)
-            else:
-                slabs = plan.slab_ranges
-                longest = max(z1 - z0 for z0, z1 in slabs)
-                nbuf = 1 if len(slabs) == 1 else 2
-                bufs = [dev.alloc((longest, grid.n_y, grid.n_x))
-                        for _ in range(nbuf)]
-                ready = [torch.cuda.Event() for _ in range(nbuf)]
-                free = [None] * nbuf
-                for si, (z0, z1) in enumerate(slabs):
-                    b = si % nbuf
-                    buf = bufs[b][:z1 - z0]
-                    nbytes = (z1 - z0) * plane * SCALAR_BYTES
-                    if free[b] is not None:
-                        dev.h2d.wait_event(free[b])
-                    ev = dev.begin(dev.h2d, "TransferIn", f"slab{si}", nbytes)
-                    with torch.cuda.stream(dev.h2d):
-                        chunk = src[z0:z1]
-                        if isinstance(chunk, np.ndarray):
-                            chunk = torch.from_numpy(chunk)
-                        buf.copy_(chunk, non_blocking=True)
-                    dev.end(ev, dev.h2d)
-                    ready[b].record(dev.h2d)
-                    dev.compute.wait_event(ready[b])
-                    ev = dev.begin(dev.compute,
-                                   "Kernel" if si == 0 else "Accumulate",
-                                   f"s{si}.c0")
-                    fwd(buf, geometry, (a0, a1), (z0, z1), acc, si > 0,
-                        dev.compute)
-                    dev.end(ev, dev.compute)
-                    fe = torch.cuda.Event()
-                    fe.record(dev.compute)
-                    free[b] = fe
-            if not on_dev:
-                out = torch.empty(acc.shape, dtype=torch.float32,
-                                  pin_memory=True)
-                dev.d2h.wait_stream(dev.compute)
-                ev = dev.begin(dev.d2h, "TransferOut", "out",
-                               acc.numel() * SCALAR_BYTES)
-                with torch.cuda.stream(dev.d2h):
-                    out.copy_(acc, non_blocking=True)
-                dev.end(ev, dev.d2h)
-                dev.d2h.synchronize()
-                parts[i] = out.numpy()
-            else:
                 parts[i] = acc
+                _join_streams(dev)
+                return
+            slabs = plan.slab_ranges
+            longest = max(z1 - z0 for z0, z1 in slabs)
+            nbuf = 1 if len(slabs) == 1 else 2
+            staging = (_Staging(2, longest * plane)
+                       if isinstance(src, np.ndarray) and not pin.ok else None)
+            window = (a1 - a0) * sheet * SCALAR_BYTES
+            slab_bytes = longest * plane * SCALAR_BYTES
+            if window + nbuf * slab_bytes <= dev.budget:
+                parts[i] = _forward_resident(dev, src, slabs, nbuf, longest,
+                                             staging, (a0, a1), on_dev)
+            else:
+                cbytes = 3 * plan.chunk_angles * sheet * SCALAR_BYTES
+                if nbuf * slab_bytes + cbytes > dev.budget:
+                    nbuf = 1  # the reference's one slab + three chunks
+                parts[i] = _forward_chunked(dev, src, slabs, nbuf, longest,
+                                            staging, (a0, a1),
+                                            plan.chunk_angles)
             _join_streams(dev)
 
-    with _Pinned(volume.data if not on_dev else None, plan.pin_host_image,
-                 host_events):
+    def _forward_resident(dev, src, slabs, nbuf, longest, staging, window,
+                          dev_out):
+        a0, a1 = window
+        acc = dev.alloc((a1 - a0, det.n_v, det.n_u))
+        bufs = [dev.alloc((longest, grid.n_y, grid.n_x)) for _ in range(nbuf)]
+        ready = [torch.cuda.Event() for _ in range(nbuf)]
+        free = [None] * nbuf
+        for si, (z0, z1) in enumerate(slabs):
+            b = si % nbuf
+            buf = bufs[b][:z1 - z0]
+            if free[b] is not None:
+                dev.h2d.wait_event(free[b])
+            ev = dev.begin(dev.h2d, "TransferIn", f"slab{si}",
+                           (z1 - z0) * plane * SCALAR_BYTES)
+            _upload(buf, src[z0:z1], dev.h2d, staging)
+            dev.end(ev, dev.h2d)
+            ready[b].record(dev.h2d)
+            dev.compute.wait_event(ready[b])
+            ev = dev.begin(dev.compute, "Kernel" if si == 0 else "Accumulate",
+                           f"s{si}.c0")
+            fwd(buf, geometry, (a0, a1), (z0, z1), acc, si > 0, dev.compute)
+            dev.end(ev, dev.compute)
+            fe = torch.cuda.Event()
+            fe.record(dev.compute)
+            free[b] = fe
+        if dev_out:
+            return acc
+        out = torch.empty(acc.shape, dtype=torch.float32, pin_memory=True)
+        dev.d2h.wait_stream(dev.compute)
+        ev = dev.begin(dev.d2h, "TransferOut", "out",
+                       acc.numel() * SCALAR_BYTES)
+        with torch.cuda.stream(dev.d2h):
+            out.copy_(acc, non_blocking=True)
+        dev.end(ev, dev.d2h)
+        dev.d2h.synchronize()
+        return out.numpy()
+
+    def _forward_chunked(dev, src, slabs, nbuf, longest, staging, window,
+                         chunk_angles):
+        """Algorithm 1 proper: the device holds slab buffers and three chunk
+        buffers; partial projections live on the host between slabs."""
+        a0, a1 = window
+        chunks = [(c, min(c + chunk_angles, a1))
+                  for c in range(a0, a1, chunk_angles)]
+        csize = chunk_angles * sheet
+        res = np.empty((a1 - a0, det.n_v, det.n_u), np.float32)
+        bufs = [dev.alloc((longest, grid.n_y, grid.n_x)) for _ in range(nbuf)]
+        cbufs = [dev.alloc((csize,)) for _ in range(3)]
+        pins = [torch.empty(csize, dtype=torch.float32, pin_memory=True)
+                for _ in range(3)]
+        slab_ready = [torch.cuda.Event() for _ in range(nbuf)]
+        slab_free = [None] * nbuf
+        cfree = [None] * 3       # compute done with a chunk buffer
+        pending = []             # (pinned idx, event, c0, c1) drains
+        k = 0
+
+        def drain(upto_len):
+            while len(pending) > upto_len:
+                pb, e, c0, c1 = pending.pop(0)
+                e.synchronize()
+                n = (c1 - c0) * sheet
+                res[c0 - a0:c1 - a0] = pins[pb][:n].numpy().reshape(
+                    c1 - c0, det.n_v, det.n_u)
+
+        for si, (z0, z1) in enumerate(slabs):
+            b = si % nbuf
+            buf = bufs[b][:z1 - z0]
+            if slab_free[b] is not None:
+                dev.h2d.wait_event(slab_free[b])
+            ev = dev.begin(dev.h2d, "TransferIn", f"slab{si}",
+                           (z1 - z0) * plane * SCALAR_BYTES)
+            _upload(buf, src[z0:z1], dev.h2d, staging)
+            dev.end(ev, dev.h2d)
+            slab_ready[b].record(dev.h2d)
+            drain(0)  # partials of slab si-1 are on the host
+            for ci, (c0, c1) in enumerate(chunks):
+                cb = k % 3
+                k += 1
+                n = (c1 - c0) * sheet
+                cbuf = cbufs[cb][:n].view(c1 - c0, det.n_v, det.n_u)
+                drain(2)  # pinned buffer cb is free once its drain is done
+                if cfree[cb] is not None:
+                    dev.h2d.wait_event(cfree[cb])
+                if si > 0:
+                    pins[cb][:n].numpy()[:] = res[c0 - a0:c1 - a0].reshape(-1)
+                    ev = dev.begin(dev.h2d, "TransferIn", f"partial{ci}",
+                                   n * SCALAR_BYTES)
+                    with torch.cuda.stream(dev.h2d):
+                        cbuf.view(-1).copy_(pins[cb][:n], non_blocking=True)
+                    dev.end(ev, dev.h2d)
+                dev.compute.wait_stream(dev.h2d)
+                dev.compute.wait_event(slab_ready[b])
+                ev = dev.begin(dev.compute,
+                               "Kernel" if si == 0 else "Accumulate",
+                               f"s{si}.c{ci}")
+                fwd(buf, geometry, (c0, c1), (z0, z1), cbuf, si > 0,
+                    dev.compute)
+                dev.end(ev, dev.compute)
+                dev.d2h.wait_stream(dev.compute)
+                ev = dev.begin(dev.d2h, "TransferOut", f"chunk{ci}",
+                               n * SCALAR_BYTES)
+                with torch.cuda.stream(dev.d2h):
+                    pins[cb][:n].copy_(cbuf.view(-1), non_blocking=True)
+                dev.end(ev, dev.d2h)
+                de = torch.cuda.Event()
+                de.record(dev.d2h)
+                cfree[cb] = de
+                pending.append((cb, de, c0, c1))
+            fe = torch.cuda.Event()
+            fe.record(dev.compute)
+            slab_free[b] = fe
+        drain(0)
+        return res
+
+    with pin:
         _run_devices(work, len(pool))
     rank, world = dist_info()
     if world > 1 and world == len(pool):
@@ -372,8 +529,8 @@ def execute_forward(volume: Volume, geometry: ScanGeometry, pool: DevicePool,
         full = _allgather_rows(t.to(dev), plan.angle_assignment, rank)
         data = full if on_dev else full.cpu().numpy()
     elif on_dev:
-        data = torch.cat([p.to(volume.data.device) for p in parts
-                          if p is not None], 0)
+        data = torch.cat([torch.as_tensor(p).to(volume.data.device)
+                          for p in parts if p is not None], 0)
     else:
         data = np.concatenate([p for p in parts if p is not None], 0)
     _finish(devs, host_events, trace_sink)
@@ -395,9 +552,16 @@ def execute_backward(projections: ProjectionStack, geometry: ScanGeometry,
                      pool: DevicePool, plan: SplitPlan,
                      mode: WeightMode = WeightMode.FDK,
                      tiles: BackwardTileSpec = BackwardTileSpec(),
-                     trace_sink: list | None = None) -> Volume:
+                     trace_sink: list | None = None,
+                     out: Volume | None = None) -> Volume:
     """Run a planned backward pass (execution.py:249-317); equals the
-    monolithic backprojection."""
+    monolithic backprojection.
+
+    Per device: when the whole projection set fits beside two slab
+    buffers it is uploaded once; otherwise every owned slab streams all
+    angle chunks through two chunk buffers (Algorithm 2 proper).  ``out``
+    (optional, host or file-backed ``fileio.create_volume``) receives the
+    result slab by slab instead of a fresh array."""
     _validate(plan, OpKind.BACKWARD, geometry, pool)
     grid, det = geometry.voxel_grid, geometry.detector
     if projections.angle_range != (0, geometry.n_angles):
@@ -407,15 +571,24 @@ def execute_backward(projections: ProjectionStack, geometry: ScanGeometry,
     slabs = backward_slabs(plan, D)
     queues = [list(range(d, len(slabs), D)) for d in range(D)]
     plane = grid.n_x * grid.n_y
-    if on_dev:
-        out = torch.zeros((grid.n_z, grid.n_y, grid.n_x), dtype=torch.float32,
+    sheet = det.n_u * det.n_v
+    if out is not None:
+        if out.grid != grid or out.slab_range != (0, grid.n_z):
+            raise ValueError("out must be a full volume on the scan grid")
+        res = out.data
+    elif on_dev:
+        res = torch.zeros((grid.n_z, grid.n_y, grid.n_x), dtype=torch.float32,
                           device=projections.data.device)
     else:
-        out = np.zeros((grid.n_z, grid.n_y, grid.n_x), np.float32)
+        res = np.zeros((grid.n_z, grid.n_y, grid.n_x), np.float32)
+    res_dev = isinstance(res, torch.Tensor) and res.is_cuda
     devs: list = [None] * D
     host_events: list = []
     bwd = K.bwd_fdk if mode is WeightMode.FDK else K.bwd_matched
     A = geometry.n_angles
+    src_all = projections.data
+    pin = _Pinned(src_all if isinstance(src_all, np.ndarray) else None,
+                  plan.pin_host_image, host_events)
 
     def work(i: int):
         if not queues[i]:
@@ -424,68 +597,113 @@ def execute_backward(projections: ProjectionStack, geometry: ScanGeometry,
         devs[i] = dev
         with torch.cuda.device(dev.cuda):
             src = projections.data
-            if on_dev and src.device == dev.cuda:
+            longest = max(slabs[q][1] - slabs[q][0] for q in queues[i])
+            nbuf = 1 if len(queues[i]) == 1 else 2
+            slab_bytes = longest * plane * SCALAR_BYTES
+            local = on_dev and src.device == dev.cuda
+            whole = local or (A * sheet * SCALAR_BYTES + nbuf * slab_bytes
+                              <= dev.budget)
+            if not whole and nbuf * slab_bytes + 2 * min(
+                    plan.chunk_angles, A) * sheet * SCALAR_BYTES > dev.budget:
+                nbuf = 1  # the reference's one slab + two chunks
+            staging = None
+            if isinstance(src, np.ndarray) and not pin.ok:
+                piece = A if whole else min(plan.chunk_angles, A)
+                staging = _Staging(2, piece * sheet)
+            proj = None
+            if local:
                 proj = src
                 dev.compute.wait_stream(torch.cuda.current_stream(dev.cuda))
-            else:
+            elif whole:
                 proj = dev.alloc(tuple(src.shape))
                 ev = dev.begin(dev.h2d, "TransferIn", "chunk.all",
                                proj.numel() * SCALAR_BYTES)
-                with torch.cuda.stream(dev.h2d):
-                    s = torch.from_numpy(src) if isinstance(src, np.ndarray) \
-                        else src
-                    proj.copy_(s, non_blocking=True)
+                _upload(proj, src, dev.h2d, staging)
                 dev.end(ev, dev.h2d)
                 dev.compute.wait_stream(dev.h2d)
-            longest = max(slabs[s][1] - slabs[s][0] for s in queues[i])
-            nbuf = 1 if len(queues[i]) == 1 else 2
+            else:
+                C = min(plan.chunk_angles, A)
+                cbufs = [dev.alloc((C * sheet,)) for _ in range(2)]
+                cdone = [None, None]
             bufs = [dev.alloc((longest, grid.n_y, grid.n_x))
                     for _ in range(nbuf)]
             drained = [None] * nbuf
             pinned_out = None
-            if not on_dev:
+            if not res_dev:
                 pinned_out = [torch.empty((longest, grid.n_y, grid.n_x),
                                           dtype=torch.float32,
                                           pin_memory=True)
                               for _ in range(nbuf)]
             pending = []
+            k = 0
             for qi, si in enumerate(queues[i]):
                 z0, z1 = slabs[si]
                 b = qi % nbuf
                 if drained[b] is not None:
                     dev.compute.wait_event(drained[b])
                     # host copy of the previous user of this buffer
-                    _flush(pending, out, b)
+                    _flush(pending, res, b)
                 buf = bufs[b][:z1 - z0]
                 with torch.cuda.stream(dev.compute):
                     buf.zero_()
-                ev = dev.begin(dev.compute, "Kernel", f"s{si}.c0")
-                bwd(proj, geometry, (0, A), (z0, z1), buf, dev.compute)
-                dev.end(ev, dev.compute)
+                if proj is not None:
+                    ev = dev.begin(dev.compute, "Kernel", f"s{si}.c0")
+                    bwd(proj, geometry, (0, A), (z0, z1), buf, dev.compute)
+                    dev.end(ev, dev.compute)
+                else:
+                    for ci, c0 in enumerate(range(0, A, C)):
+                        c1 = min(c0 + C, A)
+                        cb = k % 2
+                        k += 1
+                        cbuf = cbufs[cb][:(c1 - c0) * sheet].view(
+                            c1 - c0, det.n_v, det.n_u)
+                        if cdone[cb] is not None:
+                            dev.h2d.wait_event(cdone[cb])
+                        ev = dev.begin(dev.h2d, "TransferIn", f"chunk{ci}",
+                                       (c1 - c0) * sheet * SCALAR_BYTES)
+                        _upload(cbuf, src[c0:c1], dev.h2d, staging)
+                        dev.end(ev, dev.h2d)
+                        dev.compute.wait_stream(dev.h2d)
+                        ev = dev.begin(dev.compute, "Kernel", f"s{si}.c{ci}")
+                        bwd(cbuf, geometry, (c0, c1), (z0, z1), buf,
+                            dev.compute)
+                        dev.end(ev, dev.compute)
+                        ce = torch.cuda.Event()
+                        ce.record(dev.compute)
+                        cdone[cb] = ce
                 nbytes = (z1 - z0) * plane * SCALAR_BYTES
                 dev.d2h.wait_stream(dev.compute)
                 ev = dev.begin(dev.d2h, "TransferOut", f"slab{si}", nbytes)
                 with torch.cuda.stream(dev.d2h):
-                    if on_dev:
-                        out[z0:z1].copy_(buf, non_blocking=True)
+                    if res_dev:
+                        res[z0:z1].copy_(buf, non_blocking=True)
                     else:
                         pinned_out[b][:z1 - z0].copy_(buf, non_blocking=True)
                 dev.end(ev, dev.d2h)
                 de = torch.cuda.Event()
                 de.record(dev.d2h)
                 drained[b] = de
-                if not on_dev:
+                if not res_dev:
                     pending.append((b, de, pinned_out[b], z0, z1))
             dev.d2h.synchronize()
-            _flush(pending, out, None)
+            _flush(pending, res, None)
             _join_streams(dev)
 
-    _run_devices(work, D)
+    with pin:
+        _run_devices(work, D)
     rank, world = dist_info()
     if world > 1 and world == D:
-        out = _gather_slabs(out, slabs, queues, rank, on_dev)
+        full = _gather_slabs(res, slabs, queues, rank, res_dev)
+        if out is not None and not res_dev:
+            res[...] = full
+        else:
+            res = full
     _finish(devs, host_events, trace_sink)
-    return Volume(grid, out, (0, grid.n_z))
+    if out is not None:
+        if isinstance(out.data, np.memmap):
+            out.data.flush()
+        return out
+    return Volume(grid, res, (0, grid.n_z))
 
 
 def _flush(pending, out, only_buf):

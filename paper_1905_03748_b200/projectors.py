@@ -88,6 +88,9 @@ def _as_f32(data):
         if data.dtype != torch.float32:
             data = data.float()
         return data.contiguous()
+    if isinstance(data, np.memmap) and data.dtype == DTYPE and \
+            data.flags.c_contiguous:
+        return data  # file-backed (fileio mmap): streamed, never pinned
     return np.ascontiguousarray(data, dtype=DTYPE)
 
 
