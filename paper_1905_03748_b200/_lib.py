@@ -16,8 +16,8 @@ import numpy as np
 __all__ = ["lib", "check", "NativeLibraryError", "ConesplitCudaError",
            "LIB_PATH", "SYMBOLS", "dptr", "hptr", "stream_ptr"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
-                        "libconesplit_b200.so")
+LIB_PATH = os.environ.get("CS_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "libconesplit_b200.so")
 
 
 class NativeLibraryError(RuntimeError):

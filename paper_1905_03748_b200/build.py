@@ -19,8 +19,8 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libconesplit_b200.so")
-SOURCES = ["runtime.cu", "forward.cu", "backward.cu", "staged.cu", "tv.cu",
-           "vector.cu"]
+SOURCES = ["runtime.cu", "forward.cu", "fwd_dual.cu", "backward.cu",
+           "staged.cu", "tv.cu", "vector.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xptxas", "-v", "--expt-relaxed-constexpr"]
@@ -41,19 +41,25 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, out_dir: str = OUT_DIR,
+          defines: tuple = ()) -> str:
+    """Compile every source into out_dir/libconesplit_b200.so; ``defines``
+    (e.g. ("DUAL_MINB=1",)) build A/B variants into another out_dir."""
     nvcc = _nvcc()
-    os.makedirs(OUT_DIR, exist_ok=True)
+    os.makedirs(out_dir, exist_ok=True)
+    lib_path = os.path.join(out_dir, "libconesplit_b200.so")
+    dflags = [f"-D{d}" for d in defines]
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC)
                if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(INCLUDE, "conesplit_b200.h"))
     objs = []
     for src in SOURCES:
         path = os.path.join(CSRC, src)
-        obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
+        obj = os.path.join(out_dir, src.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, [path] + headers):
-            cmd = [nvcc, *ARCH, *FLAGS, "-I", INCLUDE, "-c", path, "-o", obj]
+            cmd = [nvcc, *ARCH, *FLAGS, *dflags, "-I", INCLUDE, "-c", path,
+                   "-o", obj]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
@@ -61,12 +67,12 @@ def build(verbose: bool = False, force: bool = False) -> str:
                 sys.stderr.write(r.stderr)
             with open(obj + ".ptxas.txt", "w") as f:
                 f.write(r.stderr)
-    if force or _stale(LIB, objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", LIB, *objs]
+    if force or _stale(lib_path, objs):
+        cmd = [nvcc, *ARCH, "-shared", "-o", lib_path, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":

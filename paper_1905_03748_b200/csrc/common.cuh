@@ -264,6 +264,15 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
                   const float* proj_in, const float* rb, const float* rw,
                   cudaStream_t s);
 
+// Ax on both fetch pipes (fwd_dual.cu): texture-gather warps and
+// shared-memory staged warps in one persistent CTA sharing a work queue.
+bool dual_enabled();
+template <int MODE>
+int launch_dual(cudaTextureObject_t tex, const float* vol,
+                const AngleGeom* dgeom, const Grid& G, double step_max,
+                int z_lo, int z_hi, int n_a, int n_u, int n_v, int v0, int v1,
+                float* out, const float* b, const float* w, cudaStream_t s);
+
 inline int num_sms() {
   static int sms = -1;
   if (sms < 0) {

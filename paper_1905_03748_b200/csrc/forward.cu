@@ -226,6 +226,20 @@ static int launch_interp(const float* vol, int nx, int ny, int nz, int z_lo,
       release_geometry(dgeom, s);
       return rc;
     }
+    if (dual_enabled()) {
+      rc = first ? launch_dual<MODE>(t->tex, vol + (size_t)(s0 - z_lo) * plane,
+                                     dgeom, G, step_max, s0, s1, n_a, n_u,
+                                     n_v, v0, v1, out, b, w, s)
+                 : launch_dual<FWD_ACCUMULATE>(
+                       t->tex, vol + (size_t)(s0 - z_lo) * plane, dgeom, G,
+                       step_max, s0, s1, n_a, n_u, n_v, v0, v1, out, nullptr,
+                       nullptr, s);
+      if (rc) {
+        release_geometry(dgeom, s);
+        return rc;
+      }
+      continue;
+    }
     auto kern = first ? fwd_interp_kernel<MODE>
                       : fwd_interp_kernel<FWD_ACCUMULATE>;
     kern<<<grid, block, 0, s>>>(t->tex, dgeom, G, step_max, s0, s1, n_u, n_v,

@@ -1,0 +1,151 @@
+"""Large-configuration measurements on ONE B200 (not the bench contract):
+
+* ``c3``: the per-rank work of config 3 (2048^3 volume, 2048^2 detector,
+  1024 views) under the paper's splits at N GPUs -- interp Ax of the rank's
+  1024/N views over the full volume (angle split) and matched Atb of all
+  1024 views into the rank's 2048/N-plane slab (slab split).  Per-rank work
+  at N = 8 is what one GPU does in the 8-GPU run (no collective sits in the
+  data path), so its GUPS bounds the 8-GPU throughput at 8x.  Also A/B of
+  v-band culling (CS_NO_CULL=1 in a second process).
+* ``ooc``: out-of-core streaming through execute_forward / execute_backward
+  with a device budget below the volume size (slabs streamed H2D from
+  page-locked host memory, Algorithm 1/2), against the same operators
+  in-core.
+
+    python tools/bench_scale.py c3 [N=8] [views=1024]
+    python tools/bench_scale.py ooc [n=2048] [views=64] [budget_gib=12]
+
+Prints one JSON line per measurement.
+"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import bench
+import paper_1905_03748_b200 as cs
+from paper_1905_03748_b200 import kernels as K
+
+
+def timed(fn, reps=1):
+    fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) * 1e-3 / reps
+
+
+def c3(N=8, A=1024, n=2048, rank=None):
+    dev = torch.device("cuda", 0)
+    rank = N // 2 if rank is None else rank   # a central slab
+    g = bench.make_geometry(n, A, cs)
+    vol = cs.phantom(cs.PhantomKind.SHEPP_LOGAN_3D, g.voxel_grid,
+                     device=dev).data
+    a0, a1 = A * rank // N, A * (rank + 1) // N
+    z0, z1 = n * rank // N, n * (rank + 1) // N
+    proj = torch.empty((a1 - a0, n, n), device=dev)
+    chunk = 64
+    t_ax = timed(lambda: [K.fwd_interp(vol, g, (c, min(c + chunk, a1)),
+                                       (0, n), proj[c - a0:min(c + chunk, a1) - a0])
+                          for c in range(a0, a1, chunk)])
+    ax_upd = float(a1 - a0) * n ** 3
+    # Atb input: a dense stack (1 + sinogram of the phantom: no zero
+    # pixels, which the matched adjoint would skip, _kernels.py:295-296)
+    y = torch.empty((A, n, n), device=dev)
+    for c in range(0, A, chunk):
+        K.fwd_interp(vol, g, (c, min(c + chunk, A)), (0, n), y[c:c + chunk])
+    y += 1.0
+    del vol
+    torch.cuda.empty_cache()
+    slab = torch.zeros((z1 - z0, n, n), device=dev)
+
+    def atb():
+        for c in range(0, A, chunk):
+            K.bwd_matched(y[c:c + chunk], g, (c, min(c + chunk, A)),
+                          (z0, z1), slab)
+    t_atb = timed(atb)
+    atb_upd = float(A) * (z1 - z0) * n * n
+    out = {"measure": "c3_rank_share", "N": N, "rank": rank, "n": n,
+           "views": A, "cull": os.environ.get("CS_NO_CULL", "0") != "1",
+           "ax_gups": ax_upd / t_ax / 1e9, "ax_s": t_ax,
+           "atb_matched_gups": atb_upd / t_atb / 1e9, "atb_s": t_atb,
+           "step_gups_per_rank": (ax_upd + atb_upd) / (t_ax + t_atb) / 1e9}
+    out["projected_N_gpu_gups"] = out["step_gups_per_rank"] * N
+    print(json.dumps(out), flush=True)
+
+
+def ooc(n=2048, A=64, budget_gib=12.0):
+    import numpy as np
+    dev = torch.device("cuda", 0)
+    g = bench.make_geometry(n, A, cs)
+    vol_d = cs.phantom(cs.PhantomKind.SHEPP_LOGAN_3D, g.voxel_grid,
+                       device=dev).data
+    IP = cs.ProjectionMethod.INTERPOLATED
+    # in-core reference timings (device-resident operators)
+    y_d = torch.empty((A, n, n), device=dev)
+    t_fwd_in = timed(lambda: K.fwd_interp(vol_d, g, (0, A), (0, n), y_d))
+    acc = torch.zeros_like(vol_d)
+    t_bwd_in = timed(lambda: K.bwd_matched(y_d, g, (0, A), (0, n), acc))
+    ref_f = y_d.cpu()
+    ref_b = None
+    acc.zero_()
+    K.bwd_matched(y_d, g, (0, A), (0, n), acc)
+    ref_b = acc.cpu()
+    # host images (page-locked by the executor per plan.pin_host_image)
+    vol_h = vol_d.cpu().numpy()
+    y_h = y_d.cpu().numpy()
+    del acc, vol_d, y_d
+    torch.cuda.empty_cache()
+    pool = cs.DevicePool((cs.DeviceSpec(memory_budget=int(budget_gib * 2 ** 30),
+                                        cuda_device=0),))
+    fplan, bplan = cs.plan_forward(g, pool), cs.plan_backward(g, pool)
+    vol = cs.Volume(g.voxel_grid, vol_h)
+    stack = cs.ProjectionStack(g.detector, y_h)
+    res = {}
+    for name, fn in (
+            ("fwd", lambda sink: cs.execute_forward(vol, g, pool, fplan, IP,
+                                                    trace_sink=sink)),
+            ("bwd", lambda sink: cs.execute_backward(
+                stack, g, pool, bplan, cs.WeightMode.MATCHED,
+                trace_sink=sink))):
+        fn(None)
+        torch.cuda.synchronize()
+        sink = []
+        t0 = time.perf_counter()
+        r = fn(sink)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        tr = sink[0]
+        ker = sum(e.end - e.start for e in tr.events
+                  if e.kind in ("Kernel", "Accumulate"))
+        h2d = sum(e.bytes for e in tr.events if e.kind == "TransferIn")
+        d2h = sum(e.bytes for e in tr.events if e.kind == "TransferOut")
+        ref = ref_f if name == "fwd" else ref_b
+        a = torch.as_tensor(np.asarray(r.data)).double()
+        rel = float((a - ref.double()).norm() / ref.double().norm())
+        res[name] = {"wall_s": dt, "kernel_s": ker,
+                     "in_core_s": t_fwd_in if name == "fwd" else t_bwd_in,
+                     "gups": A * float(n) ** 3 / dt / 1e9,
+                     "h2d_gib": h2d / 2 ** 30, "d2h_gib": d2h / 2 ** 30,
+                     "n_splits": (fplan if name == "fwd" else bplan).n_splits,
+                     "high_water_gib": max(tr.high_water.values()) / 2 ** 30,
+                     "rel_l2_vs_in_core": rel}
+    print(json.dumps({"measure": "out_of_core", "n": n, "views": A,
+                      "budget_gib": budget_gib,
+                      "volume_gib": n ** 3 * 4 / 2 ** 30, **res}), flush=True)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1]
+    args = [float(a) for a in sys.argv[2:]]
+    if what == "c3":
+        c3(*[int(a) for a in args])
+    else:
+        ooc(*([int(args[0])] if args else []) + ([int(args[1])] if len(args) > 1 else []) + (args[2:3]))
