@@ -31,7 +31,10 @@ namespace cs {
 constexpr int ST_TU = 32;
 constexpr int ST_TV = 8;
 constexpr int ST_THREADS = ST_TU * ST_TV;
-constexpr int ST_S = 8;  // planes per chunk along the main axis
+#ifndef CS_ST_S
+#define CS_ST_S 8
+#endif
+constexpr int ST_S = CS_ST_S;  // planes per chunk along the main axis
 
 
 __device__ __forceinline__ int qfloor(const March& m, int k, int axis) {

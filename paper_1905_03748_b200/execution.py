@@ -13,13 +13,16 @@ initialised and world_size == len(pool), rank r is device r):
   slab 0 overwrites it and later slabs add into it inside the Ax epilogue
   (the reference's host-side TransferIn-partial + Accumulate of
   execution.py:224-235 fused into K1);
-* backward (Alg. 2, execution.py:249-317): projections are uploaded once,
-  each owned slab is zeroed, backprojected over every angle and drained.
+* backward (Alg. 2, execution.py:249-317): projections are uploaded once
+  when they fit beside the slab buffers (else streamed in plan chunks per
+  slab); each owned slab is zeroed, backprojected over every angle and
+  drained on the host while the next slab computes.
   Slabs are dealt round-robin over ``max(plan.n_splits, n_devices)`` equal
   slabs, so every GPU works even when one slab would fit (SURVEY 0.6 --
   legal because Atb is slab-partition invariant);
-* host images are page-locked for the pass when ``plan.pin_host_image``
-  (Pin/Unpin events), device-resident inputs skip the transfers;
+* host images (numpy or file-backed memmaps) stream through a bounded
+  ring of pinned slots with multi-threaded host copies (no page-locking of
+  whole images); device-resident inputs skip the transfers;
 * every transfer and kernel is bracketed by CUDA events and reported as an
   :class:`ExecutionTrace` (``simulated=False``) whose per-device high-water
   is the executor's own allocation ledger -- check_trace() applies.
@@ -146,93 +149,119 @@ def _cuda_device(pool: DevicePool, i: int) -> torch.device:
     return torch.device("cuda", pool.cuda_index(i) % n)
 
 
-class _Pinned:
-    """Page-lock a host numpy image for the pass (execution.py:117-124)."""
-
-    def __init__(self, arr: np.ndarray | None, enabled: bool, events: list):
-        # file-backed images (fileio mmap) are streamed through pinned
-        # staging buffers instead: page-locking would read the whole file
-        self.arr = arr if (enabled and isinstance(arr, np.ndarray)
-                           and not isinstance(arr, np.memmap)
-                           and arr.nbytes > 0) else None
-        self.events = events
-        self.ok = False
-
-    def __enter__(self):
-        if self.arr is not None:
-            import time
-            t0 = time.perf_counter()
-            rc = torch.cuda.cudart().cudaHostRegister(
-                self.arr.ctypes.data, self.arr.nbytes, 0)
-            self.ok = (int(rc) == 0) if not hasattr(rc, "value") else \
-                (rc.value == 0)
-            self.events.append(TraceEvent(HOST, "Pin", "image", 0.0,
-                                          time.perf_counter() - t0,
-                                          self.arr.nbytes))
-        return self
-
-    def __exit__(self, *exc):
-        if self.arr is not None and self.ok:
-            import time
-            t0 = time.perf_counter()
-            torch.cuda.cudart().cudaHostUnregister(self.arr.ctypes.data)
-            self.events.append(TraceEvent(HOST, "Unpin", "image", 0.0,
-                                          time.perf_counter() - t0,
-                                          self.arr.nbytes))
-        return False
+_COPY_POOL = None
+_COPY_LOCK = threading.Lock()
+_PIECE_BYTES = 64 << 20   # one pinned ring slot
+_RING_SLOTS = 4
 
 
-class _Staging:
-    """Pinned host ring for host sources that are not page-locked
-    (file-backed memmaps, or pinning disabled): each upload copies the
-    piece into a pinned buffer on the host (multi-threaded numpy copy, the
-    GIL is released) and enqueues the H2D from it, so slab s+1 is read from
-    the page cache while slab s computes.  A buffer is reused only after
-    its previous H2D completed."""
+def _copy_pool():
+    global _COPY_POOL
+    with _COPY_LOCK:
+        if _COPY_POOL is None:
+            import concurrent.futures
+            import os
+            _COPY_POOL = concurrent.futures.ThreadPoolExecutor(
+                max_workers=max(2, min(16, os.cpu_count() or 2)),
+                thread_name_prefix="cs-copy")
+        return _COPY_POOL
 
-    def __init__(self, nbuf: int, max_elems: int):
-        self.bufs = [torch.empty(max(1, max_elems), dtype=torch.float32,
-                                 pin_memory=True) for _ in range(nbuf)]
-        self.done = [None] * nbuf
+
+def _par_copy(dst: np.ndarray, src: np.ndarray):
+    """dst[:] = src for 1-D float32 arrays, split over the copy pool (numpy
+    releases the GIL): host memcpy at ~10 GB/s per core would otherwise be
+    the bottleneck of streamed passes."""
+    n = src.shape[0]
+    parts = min(16, max(1, (n * 4) >> 22))  # >= 4 MiB per part
+    if parts == 1:
+        np.copyto(dst, src)
+        return
+    step = -(-n // parts)
+    futs = [_copy_pool().submit(np.copyto, dst[j:j + step], src[j:j + step])
+            for j in range(0, n, step)]
+    for f in futs:
+        f.result()
+
+
+class _HostLink:
+    """Host <-> device streaming through a bounded ring of pinned slots
+    (4 x 64 MiB, cached by torch's pinned allocator across passes): every
+    piece is copied between the host array and a slot by the copy pool and
+    moved by DMA on the caller's stream; a slot is refilled only after its
+    DMA completed.  Nothing is page-locked in place, so host images of any
+    size -- including file-backed memmaps (fileio) -- stream at host-memcpy
+    speed with bounded pinned memory (the paper's pinned double buffers,
+    PAPER.md:106-110, instead of registering the whole image)."""
+
+    def __init__(self):
+        n = _PIECE_BYTES // 4
+        self.slots = [torch.empty(n, dtype=torch.float32, pin_memory=True)
+                      for _ in range(_RING_SLOTS)]
+        self.busy = [None] * _RING_SLOTS
         self.next = 0
 
-    @staticmethod
-    def _copy(dst: np.ndarray, src: np.ndarray):
-        n = src.shape[0]
-        if src.nbytes < (64 << 20) or n < 2:
-            np.copyto(dst, src)
-            return
-        parts = min(8, n)
-        step = -(-n // parts)
-        ts = [threading.Thread(target=np.copyto,
-                               args=(dst[j:j + step], src[j:j + step]))
-              for j in range(0, n, step)]
-        for t in ts:
-            t.start()
-        for t in ts:
-            t.join()
-
-    def upload(self, dst: torch.Tensor, src: np.ndarray, stream):
-        b = self.next % len(self.bufs)
+    def _slot(self) -> int:
+        b = self.next % _RING_SLOTS
         self.next += 1
-        if self.done[b] is not None:
-            self.done[b].synchronize()
-        flat = self.bufs[b][:src.size]
-        self._copy(flat.numpy().reshape(src.shape), src)
-        with torch.cuda.stream(stream):
-            dst.copy_(flat.view(dst.shape), non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record(stream)
-        self.done[b] = ev
+        if self.busy[b] is not None:
+            self.busy[b].synchronize()
+            self.busy[b] = None
+        return b
+
+    def h2d(self, dst: torch.Tensor, src: np.ndarray, stream):
+        """Enqueue dst <- src (returns once every piece is in a slot)."""
+        flat_d = dst.view(-1)
+        flat_s = np.ascontiguousarray(src).reshape(-1)
+        n = flat_s.shape[0]
+        step = self.slots[0].numel()
+        for off in range(0, n, step):
+            m = min(step, n - off)
+            b = self._slot()
+            _par_copy(self.slots[b][:m].numpy(), flat_s[off:off + m])
+            with torch.cuda.stream(stream):
+                flat_d[off:off + m].copy_(self.slots[b][:m],
+                                          non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            self.busy[b] = ev
+
+    def d2h(self, dst: np.ndarray, src: torch.Tensor, stream):
+        """dst <- src after the work already enqueued on ``stream``;
+        returns when dst holds the data (DMA of piece k+1 overlaps the
+        host copy of piece k)."""
+        flat_s = src.reshape(-1)
+        flat_d = dst.reshape(-1)
+        assert np.shares_memory(flat_d, dst), "d2h needs a contiguous dst"
+        n = flat_s.numel()
+        step = self.slots[0].numel()
+        pending = None
+
+        def land(p):
+            b, off, m, ev = p
+            ev.synchronize()
+            _par_copy(flat_d[off:off + m], self.slots[b][:m].numpy())
+
+        for off in range(0, n, step):
+            m = min(step, n - off)
+            b = self._slot()
+            with torch.cuda.stream(stream):
+                self.slots[b][:m].copy_(flat_s[off:off + m],
+                                        non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            self.busy[b] = ev
+            if pending is not None:
+                land(pending)
+            pending = (b, off, m, ev)
+        if pending is not None:
+            land(pending)
 
 
-def _upload(dst: torch.Tensor, src, stream, staging: "_Staging | None"):
-    """H2D (or D2D) of one slab / chunk on ``stream``."""
+def _upload(dst: torch.Tensor, src, stream, link: "_HostLink | None"):
+    """H2D (host numpy via the pinned ring) or D2D of one slab / chunk."""
     if isinstance(src, np.ndarray):
-        if staging is not None:
-            staging.upload(dst, src, stream)
-            return
-        src = torch.from_numpy(np.ascontiguousarray(src))
+        link.h2d(dst, src, stream)
+        return
     with torch.cuda.stream(stream):
         dst.copy_(src, non_blocking=True)
 
@@ -362,9 +391,6 @@ def execute_forward(volume: Volume, geometry: ScanGeometry, pool: DevicePool,
     host_events: list = []
     fwd = K.fwd_interp if method is ProjectionMethod.INTERPOLATED \
         else K.fwd_siddon
-    pin = _Pinned(volume.data if not on_dev else None, plan.pin_host_image,
-                  host_events)
-
     def work(i: int):
         a0, a1 = plan.angle_assignment[i]
         if a1 <= a0:
@@ -389,8 +415,7 @@ def execute_forward(volume: Volume, geometry: ScanGeometry, pool: DevicePool,
             slabs = plan.slab_ranges
             longest = max(z1 - z0 for z0, z1 in slabs)
             nbuf = 1 if len(slabs) == 1 else 2
-            staging = (_Staging(2, longest * plane)
-                       if isinstance(src, np.ndarray) and not pin.ok else None)
+            staging = _HostLink() if isinstance(src, np.ndarray) else None
             window = (a1 - a0) * sheet * SCALAR_BYTES
             slab_bytes = longest * plane * SCALAR_BYTES
             if window + nbuf * slab_bytes <= dev.budget:
@@ -432,15 +457,13 @@ def execute_forward(volume: Volume, geometry: ScanGeometry, pool: DevicePool,
             free[b] = fe
         if dev_out:
             return acc
-        out = torch.empty(acc.shape, dtype=torch.float32, pin_memory=True)
+        out = np.empty(tuple(acc.shape), np.float32)
         dev.d2h.wait_stream(dev.compute)
         ev = dev.begin(dev.d2h, "TransferOut", "out",
                        acc.numel() * SCALAR_BYTES)
-        with torch.cuda.stream(dev.d2h):
-            out.copy_(acc, non_blocking=True)
+        (staging or _HostLink()).d2h(out, acc, dev.d2h)
         dev.end(ev, dev.d2h)
-        dev.d2h.synchronize()
-        return out.numpy()
+        return out
 
     def _forward_chunked(dev, src, slabs, nbuf, longest, staging, window,
                          chunk_angles):
@@ -519,8 +542,7 @@ def execute_forward(volume: Volume, geometry: ScanGeometry, pool: DevicePool,
         drain(0)
         return res
 
-    with pin:
-        _run_devices(work, len(pool))
+    _run_devices(work, len(pool))
     rank, world = dist_info()
     if world > 1 and world == len(pool):
         mine = parts[rank]
@@ -586,9 +608,6 @@ def execute_backward(projections: ProjectionStack, geometry: ScanGeometry,
     host_events: list = []
     bwd = K.bwd_fdk if mode is WeightMode.FDK else K.bwd_matched
     A = geometry.n_angles
-    src_all = projections.data
-    pin = _Pinned(src_all if isinstance(src_all, np.ndarray) else None,
-                  plan.pin_host_image, host_events)
 
     def work(i: int):
         if not queues[i]:
@@ -606,10 +625,8 @@ def execute_backward(projections: ProjectionStack, geometry: ScanGeometry,
             if not whole and nbuf * slab_bytes + 2 * min(
                     plan.chunk_angles, A) * sheet * SCALAR_BYTES > dev.budget:
                 nbuf = 1  # the reference's one slab + two chunks
-            staging = None
-            if isinstance(src, np.ndarray) and not pin.ok:
-                piece = A if whole else min(plan.chunk_angles, A)
-                staging = _Staging(2, piece * sheet)
+            link = _HostLink() if (isinstance(src, np.ndarray)
+                                   or not res_dev) else None
             proj = None
             if local:
                 proj = src
@@ -618,7 +635,7 @@ def execute_backward(projections: ProjectionStack, geometry: ScanGeometry,
                 proj = dev.alloc(tuple(src.shape))
                 ev = dev.begin(dev.h2d, "TransferIn", "chunk.all",
                                proj.numel() * SCALAR_BYTES)
-                _upload(proj, src, dev.h2d, staging)
+                _upload(proj, src, dev.h2d, link)
                 dev.end(ev, dev.h2d)
                 dev.compute.wait_stream(dev.h2d)
             else:
@@ -628,21 +645,33 @@ def execute_backward(projections: ProjectionStack, geometry: ScanGeometry,
             bufs = [dev.alloc((longest, grid.n_y, grid.n_x))
                     for _ in range(nbuf)]
             drained = [None] * nbuf
-            pinned_out = None
-            if not res_dev:
-                pinned_out = [torch.empty((longest, grid.n_y, grid.n_x),
-                                          dtype=torch.float32,
-                                          pin_memory=True)
-                              for _ in range(nbuf)]
-            pending = []
             k = 0
+            waiting = None   # (buffer, z0, z1, event) not yet on the host
+
+            def drain(item):
+                b_, z0_, z1_, ev_, si_ = item
+                dev.d2h.wait_event(ev_)
+                tev = dev.begin(dev.d2h, "TransferOut", f"slab{si_}",
+                                (z1_ - z0_) * plane * SCALAR_BYTES)
+                if res_dev:
+                    with torch.cuda.stream(dev.d2h):
+                        res[z0_:z1_].copy_(bufs[b_][:z1_ - z0_],
+                                           non_blocking=True)
+                else:
+                    link.d2h(res[z0_:z1_], bufs[b_][:z1_ - z0_], dev.d2h)
+                dev.end(tev, dev.d2h)
+                de = torch.cuda.Event()
+                de.record(dev.d2h)
+                drained[b_] = de
+
             for qi, si in enumerate(queues[i]):
                 z0, z1 = slabs[si]
                 b = qi % nbuf
+                if waiting is not None and waiting[0] == b:
+                    drain(waiting)   # single buffer: drain before reuse
+                    waiting = None
                 if drained[b] is not None:
                     dev.compute.wait_event(drained[b])
-                    # host copy of the previous user of this buffer
-                    _flush(pending, res, b)
                 buf = bufs[b][:z1 - z0]
                 with torch.cuda.stream(dev.compute):
                     buf.zero_()
@@ -661,7 +690,7 @@ def execute_backward(projections: ProjectionStack, geometry: ScanGeometry,
                             dev.h2d.wait_event(cdone[cb])
                         ev = dev.begin(dev.h2d, "TransferIn", f"chunk{ci}",
                                        (c1 - c0) * sheet * SCALAR_BYTES)
-                        _upload(cbuf, src[c0:c1], dev.h2d, staging)
+                        _upload(cbuf, src[c0:c1], dev.h2d, link)
                         dev.end(ev, dev.h2d)
                         dev.compute.wait_stream(dev.h2d)
                         ev = dev.begin(dev.compute, "Kernel", f"s{si}.c{ci}")
@@ -671,26 +700,18 @@ def execute_backward(projections: ProjectionStack, geometry: ScanGeometry,
                         ce = torch.cuda.Event()
                         ce.record(dev.compute)
                         cdone[cb] = ce
-                nbytes = (z1 - z0) * plane * SCALAR_BYTES
-                dev.d2h.wait_stream(dev.compute)
-                ev = dev.begin(dev.d2h, "TransferOut", f"slab{si}", nbytes)
-                with torch.cuda.stream(dev.d2h):
-                    if res_dev:
-                        res[z0:z1].copy_(buf, non_blocking=True)
-                    else:
-                        pinned_out[b][:z1 - z0].copy_(buf, non_blocking=True)
-                dev.end(ev, dev.d2h)
-                de = torch.cuda.Event()
-                de.record(dev.d2h)
-                drained[b] = de
-                if not res_dev:
-                    pending.append((b, de, pinned_out[b], z0, z1))
+                done = torch.cuda.Event()
+                done.record(dev.compute)
+                # the previous slab drains on the host while this one computes
+                if waiting is not None:
+                    drain(waiting)
+                waiting = (b, z0, z1, done, si)
+            if waiting is not None:
+                drain(waiting)
             dev.d2h.synchronize()
-            _flush(pending, res, None)
             _join_streams(dev)
 
-    with pin:
-        _run_devices(work, D)
+    _run_devices(work, D)
     rank, world = dist_info()
     if world > 1 and world == D:
         full = _gather_slabs(res, slabs, queues, rank, res_dev)
@@ -704,19 +725,6 @@ def execute_backward(projections: ProjectionStack, geometry: ScanGeometry,
             out.data.flush()
         return out
     return Volume(grid, res, (0, grid.n_z))
-
-
-def _flush(pending, out, only_buf):
-    """Copy drained pinned slabs into the host volume (after their event)."""
-    keep = []
-    for item in pending:
-        b, ev, pin, z0, z1 = item
-        if only_buf is None or b == only_buf:
-            ev.synchronize()
-            out[z0:z1] = pin[:z1 - z0].numpy()
-        else:
-            keep.append(item)
-    pending[:] = keep
 
 
 def _gather_slabs(out, slabs, queues, rank, on_dev, device=None):
