@@ -357,12 +357,23 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
       for (int j = 0; j < m; j++) {
         const FsBox b = sb[j];
         const float* pj = proj + (size_t)(a0 + j) * sheet;
-        for (int e = tid; e < b.nu * b.nv; e += FS_TX * FS_TY) {
-          const int r = e / b.nu, c = e - r * b.nu;
+        // element e = tid + 128 i -> (row r, column c): one division for
+        // the first, then an incremental walk (integer division goes
+        // through the XU pipe, the kernel's busiest)
+        constexpr int NT = FS_TX * FS_TY;
+        int r = tid / b.nu, c = tid - r * b.nu;
+        const int dr = NT / b.nu, dc = NT - dr * b.nu;
+        for (int e = tid; e < b.nu * b.nv; e += NT) {
           const int u = b.u0 + c, v = b.v0 + r;
           sbox[b.off + e] = (u >= 0 && u < n_u && v >= 0 && v < n_v)
                                 ? __ldg(pj + (size_t)v * n_u + u)
                                 : 0.f;
+          c += dc;
+          r += dr;
+          if (c >= b.nu) {
+            c -= b.nu;
+            r++;
+          }
         }
       }
       __syncthreads();
@@ -391,7 +402,9 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
             const float vv = fmaf((float)k, dvz, vfrac);
             const float fl = floorf(vv);
             const float fv = vv - fl;
-            const float* q = base + (row0 + (int)fl) * b.nu;
+            // integral fl, |fl| < 2^22: int via the 1.5 * 2^23 magic add
+            const int il = __float_as_int(fl + 12582912.f) - 0x4B400000;
+            const float* q = base + (row0 + il) * b.nu;
             const float t00 = q[0], t01 = q[1];
             const float t10 = q[b.nu], t11 = q[b.nu + 1];
             const float r0 = fmaf(fu, t01 - t00, t00);
