@@ -436,24 +436,27 @@ def run_extras(args, cs, K, g, vol, y, dev, rank, world, arange, zrange):
         v = cs.backproject_slab(cs.ProjectionStack(g.detector, y_np), g,
                                 zrange, cs.WeightMode.MATCHED)
         return p, v
-    # two warm-up calls: results are held until the next call returns, so
-    # the caching pinned-host allocator needs two sets of drain buffers
-    # before it stops calling cudaHostAlloc (steady state of a user loop)
-    for _ in range(2):
+    # warm-up calls: results are held until the next call returns, so the
+    # caching pinned-host allocator needs two sets of drain buffers before
+    # it stops calling cudaHostAlloc (steady state of a user loop)
+    for _ in range(3):
         p, v = e2e_step()
-    del p, v
     torch.cuda.synchronize()
     ne = 5
+    iters = []
     t0 = time.perf_counter()
     for _ in range(ne):
+        t1 = time.perf_counter()
         p, v = e2e_step()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        iters.append((time.perf_counter() - t1) * 1e3)
     dt = (time.perf_counter() - t0) / ne
     upd = float(a1 - a0) * n ** 3 + float(A) * (z1 - z0) * n * n
     out["e2e"] = {"value": upd / dt / 1e9, "unit": "GUPS",
                   "h2d_bytes_per_step": int(vol_np.nbytes + y_np.nbytes),
                   "d2h_bytes_per_step": int(p.data.nbytes + v.data.nbytes),
                   "ms_per_step": dt * 1e3,
+                  "iter_ms": [round(x, 1) for x in iters],
                   "api": "forward_project_slab + backproject_slab(MATCHED)"
                          " on host numpy (pinned)"}
     del vol_h, y_h

@@ -64,3 +64,19 @@ for rep in range(3):
            "api_fwd_ms": (api1 - api0) * 1e3,
            "api_bwd_ms": (api2 - api1) * 1e3}
     print(json.dumps(out), flush=True)
+
+
+# the bench's e2e loop, per-iteration times (public API, host numpy in/out)
+def e2e_step():
+    p = cs.forward_project_slab(cs.Volume(g.voxel_grid, vol_np), g, (0, A), IP)
+    v = cs.backproject_slab(cs.ProjectionStack(g.detector, y_np), g, (0, n),
+                            cs.WeightMode.MATCHED)
+    return p, v
+
+
+ts = []
+for i in range(8):
+    t0 = sync_t()
+    p_, v_ = e2e_step()
+    ts.append((sync_t() - t0) * 1e3)
+print(json.dumps({"e2e_iter_ms": ts}), flush=True)
