@@ -12,6 +12,8 @@
 // and writes u - step g / ||g|| to a second buffer; both are the tiled
 // kernel below.  ROF is one fused pass per iteration (28 B /
 // voxel-iteration) with neighbours through L1 (__ldg).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cs {
@@ -86,8 +88,10 @@ __global__ void __launch_bounds__(TV_TX * TV_TY)
   constexpr int NT = TV_TX * TV_TY;
   constexpr int UN = TV_UX * TV_UY;            // 340 u values per plane
   constexpr int UPT = (UN + NT - 1) / NT;      // per thread (2)
-  __shared__ float su[3][TV_UY][TV_UX];        // planes z, z+1, z+2 (ring)
-  __shared__ float spx[TV_PY][TV_PX], spy[TV_PY][TV_PX], spz[TV_PY][TV_PX];
+  constexpr int PN = TV_PX * TV_PY;            // 297 p values per plane
+  constexpr int PPT = (PN + NT - 1) / NT;      // per thread (2)
+  __shared__ float su[3][UN];                  // planes z, z+1, z+2 (ring)
+  __shared__ float spx[PN], spy[PN], spz[PN];
   __shared__ double sred[8];
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * TV_TX + tx;
@@ -96,79 +100,115 @@ __global__ void __launch_bounds__(TV_TX * TV_TY)
   const int ze = min(z_end, zb + TV_ZC);
   const int x = x0 + tx, y = y0 + ty;
   const bool own = x < W.nx && y < W.ny;
+  const size_t plane = (size_t)W.nx * W.ny;
   double norm = 0.0;
   if (PASS == 1) norm = sqrt(*sumsq) * scale;
   const bool skip = PASS == 1 && norm < 1e-30;  // regularization.py:148-149
   const double coef = skip ? 0.0 : step / norm;   // u -= step * g / ||g||
 
-  // u tile index (lx, ly) = global (x0 - 1 + lx, y0 - 1 + ly)
+  // Per-thread tile bookkeeping is plane-invariant: computed once.  u tile
+  // element i = (lx, ly) holds global (x0 - 1 + lx, y0 - 1 + ly); p tile
+  // element e = (lx, ly) sits at the same global position.
+  int u_off[UPT];
+  bool u_ok[UPT];
+#pragma unroll
+  for (int j = 0; j < UPT; j++) {
+    const int i = tid + j * NT;
+    const int ly = i / TV_UX, lx = i - ly * TV_UX;
+    const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
+    u_ok[j] = i < UN && gx >= 0 && gx < W.nx && gy >= 0 && gy < W.ny;
+    u_off[j] = u_ok[j] ? gy * W.nx + gx : 0;  // in-plane, < 2^31
+  }
+  int p_su[PPT];           // u-tile index of the p position
+  unsigned p_flags[PPT];   // 1: inside the window (x, y); 2: x+1 in; 4: y+1 in
+#pragma unroll
+  for (int j = 0; j < PPT; j++) {
+    const int e = tid + j * NT;
+    const int ly = e / TV_PX, lx = e - ly * TV_PX;
+    const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
+    p_su[j] = ly * TV_UX + lx;
+    unsigned f = 0;
+    if (e < PN && gx >= 0 && gy >= 0 && gx < W.nx && gy < W.ny) {
+      f = 1u;
+      if (gx < W.nx - 1) f |= 2u;
+      if (gy < W.ny - 1) f |= 4u;
+    }
+    p_flags[j] = f;
+  }
+  const int own_off = own ? y * W.nx + x : 0;
+  const int c_p = (ty + 1) * TV_PX + (tx + 1);  // own p / u positions
+  const int c_u = (ty + 1) * TV_UX + (tx + 1);
+
   auto fetch = [&](int z, float (&r)[UPT]) {
+    const bool zin = z >= 0 && z < W.nz;
+    const float* uz = u + (size_t)(zin ? z : 0) * plane;
+#pragma unroll
+    for (int j = 0; j < UPT; j++)
+      r[j] = (zin && u_ok[j]) ? __ldg(uz + u_off[j]) : 0.f;
+  };
+  auto put = [&](float* dst, const float (&r)[UPT]) {
 #pragma unroll
     for (int j = 0; j < UPT; j++) {
       const int i = tid + j * NT;
-      const int ly = i / TV_UX, lx = i - ly * TV_UX;
-      const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
-      r[j] = (i < UN && z >= 0 && z < W.nz && gx >= 0 && gx < W.nx &&
-              gy >= 0 && gy < W.ny)
-                 ? __ldg(u + W.at(gx, gy, z))
-                 : 0.f;
+      if (i < UN) dst[i] = r[j];
     }
   };
-  auto put = [&](int slot, const float (&r)[UPT]) {
-#pragma unroll
-    for (int j = 0; j < UPT; j++) {
-      const int i = tid + j * NT;
-      if (i < UN) (&su[slot][0][0])[i] = r[j];
-    }
-  };
+  float* pl0 = su[0];  // plane z
+  float* pl1 = su[1];  // plane z + 1
+  float* pl2 = su[2];  // plane z + 2
   float rb[UPT];
   fetch(zb - 1, rb);
-  put(0, rb);
+  put(pl0, rb);
   fetch(zb, rb);
-  put(1, rb);
+  put(pl1, rb);
   fetch(zb + 1, rb);  // in flight while plane zb - 1 is processed
   float pz_prev = 0.f;
   double acc = 0.0;
-  int s0 = 0;  // ring slot of plane z
   for (int z = zb - 1; z < ze; z++) {
-    const int s1 = s0 == 2 ? 0 : s0 + 1, s2 = s1 == 2 ? 0 : s1 + 1;
     __syncthreads();  // planes z, z+1 visible; previous p consumed
-    for (int e = tid; e < TV_PX * TV_PY; e += NT) {
-      const int ly = e / TV_PX, lx = e - ly * TV_PX;
-      const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
+    const bool zlast = z >= W.nz - 1;
+#pragma unroll
+    for (int j = 0; j < PPT; j++) {
+      const int e = tid + j * NT;
+      if (j * NT + NT > PN && e >= PN) break;
       float px = 0.f, py = 0.f, pz = 0.f;
-      if (gx >= 0 && gy >= 0 && z >= 0 && gx < W.nx && gy < W.ny) {
-        const float cc = su[s0][ly][lx];
-        const float gxv = gx < W.nx - 1 ? su[s0][ly][lx + 1] - cc : 0.f;
-        const float gyv = gy < W.ny - 1 ? su[s0][ly + 1][lx] - cc : 0.f;
-        const float gzv = z < W.nz - 1 ? su[s1][ly][lx] - cc : 0.f;
+      const unsigned f = p_flags[j];
+      if ((f & 1u) && z >= 0) {
+        const int k = p_su[j];
+        const float cc = pl0[k];
+        const float gxv = (f & 2u) ? pl0[k + 1] - cc : 0.f;
+        const float gyv = (f & 4u) ? pl0[k + TV_UX] - cc : 0.f;
+        const float gzv = zlast ? 0.f : pl1[k] - cc;
         const float inv =
             rsqrtf(gxv * gxv + gyv * gyv + gzv * gzv + (float)TV_EPS);
         px = gxv * inv;
         py = gyv * inv;
         pz = gzv * inv;
       }
-      spx[ly][lx] = px;
-      spy[ly][lx] = py;
-      spz[ly][lx] = pz;
+      spx[e] = px;
+      spy[e] = py;
+      spz[e] = pz;
     }
-    put(s2, rb);  // plane z + 2 (slot freed by plane z - 1)
+    put(pl2, rb);  // plane z + 2 (slot freed by plane z - 1)
     if (z + 3 <= ze) fetch(z + 3, rb);
     __syncthreads();
-    const float pz_own = spz[ty + 1][tx + 1];
+    const float pz_own = spz[c_p];
     if (z >= zb && own) {
-      const float g = -((pz_own - pz_prev) +
-                        (spy[ty + 1][tx + 1] - spy[ty][tx + 1]) +
-                        (spx[ty + 1][tx + 1] - spx[ty + 1][tx]));
+      const float g = -((pz_own - pz_prev) + (spy[c_p] - spy[c_p - TV_PX]) +
+                        (spx[c_p] - spx[c_p - 1]));
       if (PASS == 0) {
         acc += (double)g * (double)g;
       } else {
-        const float uc = su[s0][ty + 1][tx + 1];
-        uo[W.at(x, y, z)] = skip ? uc : (float)((double)uc - coef * (double)g);
+        const float uc = pl0[c_u];
+        uo[(size_t)z * plane + own_off] =
+            skip ? uc : (float)((double)uc - coef * (double)g);
       }
     }
     pz_prev = pz_own;
-    s0 = s1;
+    float* t = pl0;
+    pl0 = pl1;
+    pl1 = pl2;
+    pl2 = t;
   }
   if (PASS == 0) {
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
