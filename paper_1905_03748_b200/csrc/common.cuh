@@ -235,6 +235,9 @@ int load_layered(TexRole role, const float* src, int w, int h, int layers,
 // Max layers of a 2D layered texture on this device (2048 on sm_100).
 int max_layers();
 
+// Default mempool keeps freed memory (see runtime.cu).
+void retain_pool();
+
 // Geometry tables copied to the device (stream-ordered allocation).
 int upload_geometry(const double* geom, int n_a, cudaStream_t s,
                     AngleGeom** d_geom);

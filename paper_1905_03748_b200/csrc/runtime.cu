@@ -124,8 +124,25 @@ int load_layered(TexRole role, const float* src, int w, int h, int layers,
   return CS_OK;
 }
 
+// Keep memory freed by cudaFreeAsync in the device's default pool instead
+// of returning it to the driver at every synchronisation (release threshold
+// 0 by default): the per-call geometry tables / reduction partials are then
+// sub-allocations, not fresh mappings (ms-scale jitter on small kernels).
+void retain_pool() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
+
 int upload_geometry(const double* geom, int n_a, cudaStream_t s,
                     AngleGeom** d_geom) {
+  retain_pool();
   static_assert(sizeof(AngleGeom) == 12 * sizeof(double), "layout");
   size_t bytes = (size_t)n_a * sizeof(AngleGeom);
   CS_CHECK_CUDA(cudaMallocAsync((void**)d_geom, bytes, s));

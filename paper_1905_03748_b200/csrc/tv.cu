@@ -330,6 +330,7 @@ int cs_tv_grad_sumsq(const float* u, int nx, int ny, int nzw, int core_lo,
                   (core_hi - core_lo + TV_ZC - 1) / TV_ZC);
   const size_t nb = (size_t)grid.x * grid.y * grid.z;
   double* part = nullptr;
+  retain_pool();
   CS_CHECK_CUDA(cudaMallocAsync((void**)&part, nb * sizeof(double), s));
   tv_gd_tiled_kernel<0><<<grid, dim3(TV_TX, TV_TY), 0, s>>>(
       u, nullptr, Win{nx, ny, nzw}, core_lo, core_hi, 0.0, nullptr, 1.0, part);
@@ -386,6 +387,7 @@ int cs_tv_norm(const float* u, int nx, int ny, int nzw, double* out_sum,
   const dim3 grid((nx + 31) / 32, (ny + 7) / 8, nzw);
   const size_t nb = (size_t)grid.x * grid.y * grid.z;
   double* part = nullptr;
+  retain_pool();
   CS_CHECK_CUDA(cudaMallocAsync((void**)&part, nb * sizeof(double), s));
   tv_norm_kernel<<<grid, dim3(32, 8), 0, s>>>(u, Win{nx, ny, nzw}, part);
   CS_CHECK_CUDA(cudaGetLastError());

@@ -155,3 +155,4 @@ def test_culling_is_bit_identical_subprocess():
         else:
             # matched: cross-CTA fp32 reductions are order-dependent
             assert rel_l2(a, b) <= 1e-6
+

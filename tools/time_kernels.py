@@ -46,15 +46,17 @@ if only:
     ops = {k: v for k, v in ops.items() if k in only.split(",")}
 out = {}
 for name, fn in ops.items():
-    fn()
+    for _ in range(3 if name in ("tv_gd_iter", "rof_iter") else 1):
+        fn()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(True), torch.cuda.Event(True)
     s.record()
-    for _ in range(R):
+    reps = R * 10 if name in ("tv_gd_iter", "rof_iter") else R
+    for _ in range(reps):
         fn()
     e.record()
     torch.cuda.synchronize()
-    t = s.elapsed_time(e) / R * 1e-3
+    t = s.elapsed_time(e) / reps * 1e-3
     if name in ("tv_gd_iter", "rof_iter"):
         bpv = 12.0 if name == "tv_gd_iter" else 28.0
         out[name] = {"ms": t * 1e3, "gvox_per_s": n ** 3 / t / 1e9,
