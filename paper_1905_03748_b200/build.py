@@ -19,7 +19,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libconesplit_b200.so")
-SOURCES = ["runtime.cu", "forward.cu", "fwd_dual.cu", "backward.cu",
+SOURCES = ["runtime.cu", "forward.cu", "backward.cu",
            "staged.cu", "tv.cu", "vector.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

@@ -2,11 +2,9 @@
 // interpolated projector (K2) and the voxel-driven FDK backprojector (K3).
 //
 // K2 replaces the reference's single-threaded scatter
-// (_kernels.py:278-337): one thread per ray replays K1's ray set-up and
-// sample lattice bit-for-bit (shared code in common.cuh) and scatters
-// proj*step*w_corner with fp32 reductions (RED.ADD.F32) into the slab.
-// Consecutive samples that share a base voxel are merged in registers
-// before they hit L2, which halves the reduction count along the ray.
+// (_kernels.py:278-337): the staged shared-memory kernel of staged.cu
+// replays K1's ray set-up and sample lattice exactly (shared code in
+// common.cuh); cs_bwd_matched below is its C-ABI entry.
 //
 // K3 replaces fdk_backward_chunk (_kernels.py:340-398): one thread per
 // (x, y) column and FDK_ZB consecutive z voxels held in registers; the
@@ -21,179 +19,6 @@
 #include "common.cuh"
 
 namespace cs {
-
-__device__ __forceinline__ void red_add(float* p, float v) {
-  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-
-// One 16-byte vector reduction (REDG.E.ADD.F32x4) on an aligned group.
-__device__ __forceinline__ void red_add4(float* p, float a, float b, float c,
-                                         float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p),
-               "f"(a), "f"(b), "f"(c), "f"(d)
-               : "memory");
-}
-
-// Adds (c0, c1) at x = bx, bx + 1 of one row (row 16-byte aligned, nx % 4
-// == 0).  Both taps usually sit in one aligned float4 group -> one vector
-// reduction (zeros elsewhere); otherwise per-tap scalar reductions.
-__device__ __forceinline__ void red_pair(float* row, int bx, int nx, float c0,
-                                         float c1) {
-  const int lane = bx & 3;
-  if (bx >= 0 && lane <= 2 && bx + 1 < nx) {
-    float v[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int i = 0; i < 3; i++) {
-      if (i == lane) {
-        v[i] = c0;
-        v[i + 1] = c1;
-      }
-    }
-    red_add4(row + (bx - lane), v[0], v[1], v[2], v[3]);
-    return;
-  }
-  if (bx >= 0 && bx < nx) red_add(row + bx, c0);
-  if (bx + 1 >= 0 && bx + 1 < nx) red_add(row + bx + 1, c1);
-}
-
-// Per-thread write-combining window in shared memory: a ray's taps land in
-// the 2 (z) x 2 (y) x 8 (x) voxels around its current cell, addressed
-// circularly (slot = ((z & 1) * 2 + (y & 1)) * 8 + (x & 7)) so the window
-// slides with the ray without moving data.  A row segment is flushed to
-// global memory -- one 16-byte vector reduction per aligned x-quad -- only
-// when the ray leaves it: along x every 4 planes, along y / z when the
-// cell's row changes.  This cuts L2 reduction requests ~3x against
-// flushing every cell (the measured limiter: lts tag lookups ~77%).
-// Layout [slot][thread]: every lane owns its own bank (conflict-free).
-constexpr int MW_SLOTS = 32;
-constexpr int MW_THREADS = 128;
-
-template <bool V4>
-__device__ __forceinline__ void mw_flush_quad(float* my, float* vol, int gx,
-                                              int y, int z, int nx, int ny,
-                                              int z_lo, int z_hi,
-                                              size_t plane) {
-  const int base = (((z & 1) << 1) | (y & 1)) * 8 + (gx & 7);
-  float q[4];
-#pragma unroll
-  for (int i = 0; i < 4; i++) {
-    q[i] = my[(base + i) * MW_THREADS];
-    my[(base + i) * MW_THREADS] = 0.f;
-  }
-  if (q[0] == 0.f && q[1] == 0.f && q[2] == 0.f && q[3] == 0.f) return;
-  if (z < z_lo || z >= z_hi || y < 0 || y >= ny) return;  // masked taps
-  float* row = vol + (size_t)(z - z_lo) * plane + (size_t)y * nx;
-  if (V4 && gx >= 0 && gx + 3 < nx) {
-    red_add4(row + gx, q[0], q[1], q[2], q[3]);
-    return;
-  }
-#pragma unroll
-  for (int i = 0; i < 4; i++) {
-    const int x = gx + i;
-    if (x >= 0 && x < nx && q[i] != 0.f) red_add(row + x, q[i]);
-  }
-}
-
-template <bool V4>
-__global__ void __launch_bounds__(MW_THREADS)
-    bwd_matched_kernel(float* __restrict__ vol,
-                       const AngleGeom* __restrict__ geom, Grid G,
-                       double step_max, int z_lo, int z_hi, int n_u, int n_v,
-                       const float* __restrict__ proj) {
-  extern __shared__ float mw_win[];
-  float* my = mw_win + threadIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int u = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
-  const int v = blockIdx.y * 8 + (warp >> 1) * 4 + (lane >> 3);
-  const int a = blockIdx.z;
-  if (u >= n_u || v >= n_v) return;
-  const float val = __ldg(proj + ((size_t)a * n_v + v) * n_u + u);
-  if (val == 0.f) return;  // _kernels.py:295-296
-  Ray r;
-  setup_ray(geom[a], G, step_max, u, v, r);
-  if (r.n <= 0) return;
-  March m;
-  march_params(r, G, m);
-  long long k0l, k1l;
-  slab_k_range(r, m, G, z_lo, z_hi, k0l, k1l);
-  const int k0 = (int)k0l, k1 = (int)k1l, kc = (int)m.kc;
-  if (k0 >= k1) return;
-  const int nx = G.n[0], ny = G.n[1];
-  const size_t plane = (size_t)nx * ny;
-  const float scaled = val * (float)r.step;
-#pragma unroll
-  for (int i = 0; i < MW_SLOTS; i++) my[i * MW_THREADS] = 0.f;
-
-  auto flush_row = [&](int xa, int y, int z) {
-    mw_flush_quad<V4>(my, vol, xa, y, z, nx, ny, z_lo, z_hi, plane);
-    mw_flush_quad<V4>(my, vol, xa + 4, y, z, nx, ny, z_lo, z_hi, plane);
-  };
-  auto flush_xquad = [&](int gx, int ya, int za) {
-#pragma unroll
-    for (int i = 0; i < 4; i++)
-      mw_flush_quad<V4>(my, vol, gx, ya + (i & 1), za + (i >> 1), nx, ny,
-                        z_lo, z_hi, plane);
-  };
-  const bool x_up = m.B[0] >= 0.f;
-  int xa = 0, ya = 0, za = 0;  // window base
-  bool started = false;
-  for (int k = k0; k < k1; ++k) {
-    const float kf = (float)(k - kc);
-    const float qx = fmaf(kf, m.B[0], m.A[0]);
-    const float qy = fmaf(kf, m.B[1], m.A[1]);
-    const float qz = fmaf(kf, m.B[2], m.A[2]);
-    const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
-    const float wx = qx - fx, wy = qy - fy, wz = qz - fz;
-    const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
-    if (!started) {
-      xa = x_up ? (ix & ~3) : (((ix + 1) & ~3) - 4);
-      ya = iy;
-      za = iz;
-      started = true;
-    } else {
-      // the sample step is <= half a voxel: cells move by <= 1 per axis
-      if (iz != za) {
-        const int zo = iz > za ? za : za + 1;  // plane the ray left
-        flush_row(xa, ya, zo);
-        flush_row(xa, ya + 1, zo);
-        za = iz;
-      }
-      if (iy != ya) {
-        const int yo = iy > ya ? ya : ya + 1;
-        flush_row(xa, yo, za);
-        flush_row(xa, yo, za + 1);
-        ya = iy;
-      }
-      if (ix + 1 >= xa + 8) {
-        flush_xquad(xa, ya, za);
-        xa += 4;
-      } else if (ix < xa) {
-        flush_xquad(xa + 4, ya, za);
-        xa -= 4;
-      }
-    }
-    const float z0 = scaled * (1.f - wz), z1 = scaled * wz;
-    const float w00 = z0 * (1.f - wy), w01 = z0 * wy;
-    const float w10 = z1 * (1.f - wy), w11 = z1 * wy;
-    const int x0 = ix & 7, x1 = (ix + 1) & 7;
-    const int r00 = (((iz & 1) << 1) | (iy & 1)) * 8;
-    const int r01 = r00 ^ 8;   // y + 1 flips the y parity bit
-    const int r10 = r00 ^ 16;  // z + 1 flips the z parity bit
-    const int r11 = r00 ^ 24;
-    my[(r00 + x0) * MW_THREADS] += w00 * (1.f - wx);
-    my[(r00 + x1) * MW_THREADS] += w00 * wx;
-    my[(r01 + x0) * MW_THREADS] += w01 * (1.f - wx);
-    my[(r01 + x1) * MW_THREADS] += w01 * wx;
-    my[(r10 + x0) * MW_THREADS] += w10 * (1.f - wx);
-    my[(r10 + x1) * MW_THREADS] += w10 * wx;
-    my[(r11 + x0) * MW_THREADS] += w11 * (1.f - wx);
-    my[(r11 + x1) * MW_THREADS] += w11 * wx;
-  }
-  flush_row(xa, ya, za);
-  flush_row(xa, ya + 1, za);
-  flush_row(xa, ya, za + 1);
-  flush_row(xa, ya + 1, za + 1);
-}
 
 constexpr int FDK_ZB = 16;  // z voxels per thread (registers)
 
@@ -490,32 +315,11 @@ int cs_bwd_matched(float* vol_acc, int nx, int ny, int nz, int z_lo,
   CS_REQUIRE(n_a > 0 && n_a <= 65535 && n_u > 0 && n_v > 0, CS_ERR_ARG,
              "bad projection shape");
   CS_REQUIRE(step_max > 0.0, CS_ERR_ARG, "step_max must be positive");
-  cudaStream_t s = (cudaStream_t)stream;
-  static const char* staged_knob = getenv("CS_MATCHED_WINDOW");
-  if (!(staged_knob && staged_knob[0] == '1'))  // production: staged boxes
-    return launch_staged<OP_BWD, 0>(nullptr, vol_acc, nx, ny, nz, z_lo, z_hi,
-                                    grid6, geom, n_a, n_u, n_v, step_max,
-                                    nullptr, proj, nullptr, nullptr, s);
-  const Grid G = make_grid(grid6, nx, ny, nz);
-  AngleGeom* dgeom = nullptr;
-  int rc = upload_geometry(geom, n_a, s, &dgeom);
-  if (rc) return rc;
-  const dim3 grid((n_u + 15) / 16, (n_v + 7) / 8, n_a);
-  // vector reductions need 16-byte aligned rows
-  static const char* knob = getenv("CS_MATCHED_SCALAR");
-  const bool v4 = (nx % 4 == 0) && (((uintptr_t)vol_acc & 15) == 0) &&
-                  !(knob && knob[0] == '1');
-  const size_t smem = sizeof(float) * MW_SLOTS * MW_THREADS;
-  if (v4)
-    bwd_matched_kernel<true><<<grid, MW_THREADS, smem, s>>>(
-        vol_acc, dgeom, G, step_max, z_lo, z_hi, n_u, n_v, proj);
-  else
-    bwd_matched_kernel<false><<<grid, MW_THREADS, smem, s>>>(
-        vol_acc, dgeom, G, step_max, z_lo, z_hi, n_u, n_v, proj);
-  cudaError_t e = cudaGetLastError();
-  release_geometry(dgeom, s);
-  CS_CHECK_CUDA(e);
-  return CS_OK;
+  // staged shared-memory boxes (staged.cu)
+  return launch_staged<OP_BWD, 0>(nullptr, vol_acc, nx, ny, nz, z_lo, z_hi,
+                                  grid6, geom, n_a, n_u, n_v, step_max,
+                                  nullptr, proj, nullptr, nullptr,
+                                  (cudaStream_t)stream);
 }
 
 int cs_bwd_fdk(float* vol_acc, int nx, int ny, int z_lo, int n_slab,

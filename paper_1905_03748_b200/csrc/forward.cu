@@ -5,7 +5,7 @@
 // detector tile (a compact ray frustum, so the 32 lanes gather from a
 // compact texel neighbourhood), four warps per CTA (16u x 8v).  The ray
 // set-up is fp64 and bit-identical to the reference (_kernels.py:194-246);
-// the march is fp32 with q(k) = A + (k - kc) B.  Each trilinear sample is
+// positions are exact Q32.32 fixed point (common.cuh).  Each trilinear sample is
 // TWO texture gathers (tld4 on a 2D-layered float texture: 2x2 texels of
 // slice iz and of slice iz+1) with fp32 software weights, i.e. exact
 // interpolation weights (hardware filtering's 8-bit weights are 100x off
@@ -14,6 +14,7 @@
 // x/y; z taps are masked to the slab [z_lo, z_hi) exactly as
 // _kernels.py:259-262, and the sample range is clipped to the slab so a
 // slab launch costs only its share of the ray.
+#include <climits>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -33,8 +34,11 @@ __device__ __forceinline__ void tile_coords(int& u, int& v, int v_base) {
   v = v_base + blockIdx.y * FWD_TILE_V + (warp >> 1) * 4 + (lane >> 3);
 }
 
+#ifndef FWD_MINB
+#define FWD_MINB 8  // <= 64 registers: 32 warps/SM keep the tld4 pipe fed
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, FWD_MINB)
     fwd_interp_kernel(cudaTextureObject_t tex,
                       const AngleGeom* __restrict__ geom, Grid G,
                       double step_max, int z_lo, int z_hi, int n_u, int n_v,
@@ -53,30 +57,30 @@ __global__ void __launch_bounds__(128)
     march_params(r, G, m);
     long long k0l, k1l;
     slab_k_range(r, m, G, z_lo, z_hi, k0l, k1l);
-    const int k0 = (int)k0l, k1 = (int)k1l, kc = (int)m.kc;
+    const int k0 = (int)k0l, k1 = (int)k1l;
     const int top = z_hi - z_lo - 1;
+    // exact fixed-point positions (common.cuh), advanced by integer adds
+    long long qx = q_at(m, k0, 0), qy = q_at(m, k0, 1), qz = q_at(m, k0, 2);
+    const long long bx = m.Bq[0], by = m.Bq[1], bz = m.Bq[2];
     // Consecutive samples (step <= half a voxel) often share their 2x2x2
     // texel cell; re-gather only when the cell changes (-10% texture
     // writeback, the measured limiter).
-    float cfx = -1e30f, cfy = 0.f, cfz = 0.f;
+    int cx = INT_MIN, cy = 0, cz = 0;
     float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
 #pragma unroll 2
-    for (int k = k0; k < k1; ++k) {
-      const float kf = (float)(k - kc);
-      const float qx = fmaf(kf, m.B[0], m.A[0]);
-      const float qy = fmaf(kf, m.B[1], m.A[1]);
-      const float qz = fmaf(kf, m.B[2], m.A[2]);
-      const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
-      const float wx = qx - fx, wy = qy - fy, wz = qz - fz;
-      const int l0 = (int)fz - z_lo, l1 = l0 + 1;
+    for (int k = k0; k < k1; ++k, qx += bx, qy += by, qz += bz) {
+      const int ix = q_cell(qx), iy = q_cell(qy), iz = q_cell(qz);
+      const float wx = q_frac(qx), wy = q_frac(qy), wz = q_frac(qz);
+      const int l0 = iz - z_lo, l1 = l0 + 1;
       const float m0 = (l0 >= 0 && l0 <= top) ? 1.f - wz : 0.f;
       const float m1 = (l1 >= 0 && l1 <= top) ? wz : 0.f;
-      if (fx != cfx || fy != cfy || fz != cfz) {
-        s0 = gather_a2d(tex, min(max(l0, 0), top), fx + 1.f, fy + 1.f);
-        s1 = gather_a2d(tex, min(max(l1, 0), top), fx + 1.f, fy + 1.f);
-        cfx = fx;
-        cfy = fy;
-        cfz = fz;
+      if (ix != cx || iy != cy || iz != cz) {
+        const float tx = int_to_float(ix + 1), ty = int_to_float(iy + 1);
+        s0 = gather_a2d(tex, min(max(l0, 0), top), tx, ty);
+        s1 = gather_a2d(tex, min(max(l1, 0), top), tx, ty);
+        cx = ix;
+        cy = iy;
+        cz = iz;
       }
       // s.w=(i,j) s.z=(i+1,j) s.x=(i,j+1) s.y=(i+1,j+1)
       const float r00 = fmaf(wx, s0.z - s0.w, s0.w);
@@ -225,20 +229,6 @@ static int launch_interp(const float* vol, int nx, int ny, int nz, int z_lo,
                            ny, s1 - s0, s, &t))) {
       release_geometry(dgeom, s);
       return rc;
-    }
-    if (dual_enabled()) {
-      rc = first ? launch_dual<MODE>(t->tex, vol + (size_t)(s0 - z_lo) * plane,
-                                     dgeom, G, step_max, s0, s1, n_a, n_u,
-                                     n_v, v0, v1, out, b, w, s)
-                 : launch_dual<FWD_ACCUMULATE>(
-                       t->tex, vol + (size_t)(s0 - z_lo) * plane, dgeom, G,
-                       step_max, s0, s1, n_a, n_u, n_v, v0, v1, out, nullptr,
-                       nullptr, s);
-      if (rc) {
-        release_geometry(dgeom, s);
-        return rc;
-      }
-      continue;
     }
     auto kern = first ? fwd_interp_kernel<MODE>
                       : fwd_interp_kernel<FWD_ACCUMULATE>;

@@ -17,9 +17,9 @@
 //     CAS loops on sm_100) in fixed point, scaled per CTA by its largest
 //     |proj| so no voxel sum can overflow; the box is then added to global
 //     memory with one 16-byte RED per aligned x-quad.
-// Samples, weights and masks are exactly those of the tex / register
-// kernels (same fp64 ray set-up, same fp32 lattice q(k) = A + (k - kc) B),
-// so chunking changes only summation order.  Boxes that would not fit the
+// Samples, weights and masks are exactly those of the texture kernel (same
+// fp64 ray set-up, same exact fixed-point positions q(k) = A0 + k Bq), so
+// chunking changes only summation order.  Boxes that would not fit the
 // shared-memory budget are served from global memory for that chunk.
 #include <cstdlib>
 #include <cstring>
@@ -39,15 +39,15 @@ constexpr int ST_S = CS_ST_S;  // planes per chunk along the main axis
 
 // Float -> int without the conversion pipe: for |x| < 2^22, x + 1.5 * 2^23
 // holds round-to-nearest(x) in its low mantissa bits.  F2I / FRND run at a
-// quarter of the FMA rate on sm_100 and the matched deposit needed 11 of
-// them per sample (8 taps + 3 cell indices); this is one FFMA/FADD + IADD.
+// quarter of the FMA rate on sm_100 and the matched deposit needed 8 of
+// them per sample for its fixed-point taps; this is one FFMA + IADD.
 constexpr float ST_MAGIC = 12582912.f;
 __device__ __forceinline__ int magic_int(float biased) {
   return __float_as_int(biased) - 0x4B400000;
 }
 
 __device__ __forceinline__ int qfloor(const March& m, int k, int axis) {
-  return (int)floorf(fmaf((float)(k - (int)m.kc), m.B[axis], m.A[axis]));
+  return q_cell(q_at(m, k, axis));  // exact (common.cuh)
 }
 
 // Red of a float4 quad (16-byte aligned) -- see backward.cu.
@@ -149,13 +149,10 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
     // rays of this tile march both ways along M (degenerate geometry):
     // serve every sample from global memory, no staging
     for (int kk = k0; kk < k1; kk++) {
-      const float kf = (float)(kk - (int)m.kc);
-      const float qx = fmaf(kf, m.B[0], m.A[0]);
-      const float qy = fmaf(kf, m.B[1], m.A[1]);
-      const float qz = fmaf(kf, m.B[2], m.A[2]);
-      const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
-      const float wx = qx - fx, wy = qy - fy, wz = qz - fz;
-      const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
+      const long long qx = q_at(m, kk, 0), qy = q_at(m, kk, 1),
+                      qz = q_at(m, kk, 2);
+      const float wx = q_frac(qx), wy = q_frac(qy), wz = q_frac(qz);
+      const int ix = q_cell(qx), iy = q_cell(qy), iz = q_cell(qz);
 #pragma unroll
       for (int cz = 0; cz < 2; cz++) {
         const int zi = iz + cz;
@@ -336,16 +333,12 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
     }
     // ---- samples of the chunk
     if (any) {
-      for (int kk = ka; kk < kb; kk++) {
-        const float kf = (float)(kk - (int)m.kc);
-        const float qx = fmaf(kf, m.B[0], m.A[0]);
-        const float qy = fmaf(kf, m.B[1], m.A[1]);
-        const float qz = fmaf(kf, m.B[2], m.A[2]);
-        const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
-        const float wx = qx - fx, wy = qy - fy, wz = qz - fz;
-        // fx.. are integral floats (|.| < 2^22): exact via the magic add
-        const int ix = magic_int(fx + ST_MAGIC), iy = magic_int(fy + ST_MAGIC),
-                  iz = magic_int(fz + ST_MAGIC);
+      // exact fixed-point positions (common.cuh), integer-advanced
+      long long qx = q_at(m, ka, 0), qy = q_at(m, ka, 1), qz = q_at(m, ka, 2);
+      for (int kk = ka; kk < kb;
+           kk++, qx += m.Bq[0], qy += m.Bq[1], qz += m.Bq[2]) {
+        const float wx = q_frac(qx), wy = q_frac(qy), wz = q_frac(qz);
+        const int ix = q_cell(qx), iy = q_cell(qy), iz = q_cell(qz);
         if (fits) {
           const int b = (iz - bo[2]) * sz + (iy - bo[1]) * sy +
                         (ix - bo[0]) * sx;
