@@ -477,6 +477,30 @@ def run_extras(args, cs, K, g, vol, y, dev, rank, world, arange, zrange):
         out["os_sart_s_per_iter"] = (ts[3] - ts[1]) / 2
         out["os_sart_setup_plus_1iter_s"] = ts[1]
 
+        # Config 1 loops end to end through the public API (host numpy in,
+        # host numpy out), the reference's own timing case (BASELINE.md
+        # section 2: SIRT 10 it 15.13 s, CGLS 10 it 15.66 s on 8 cores)
+        g1 = make_geometry(64, 100, cs)
+        x1 = cs.phantom(cs.PhantomKind.SHEPP_LOGAN_3D, g1.voxel_grid).data
+        b1 = cs.forward_project_slab(cs.Volume(g1.voxel_grid, x1), g1,
+                                     (0, 100),
+                                     cs.ProjectionMethod.INTERPOLATED)
+        loops = {}
+        for name, fn in (
+                ("sirt_10it_s", lambda: cs.os_sart(b1, g1, cs.ReconConfig(
+                    pool, cs.Algorithm.OSSART, 10, 100))),
+                ("cgls_10it_s", lambda: cs.cgls(b1, g1, cs.ReconConfig(
+                    pool, cs.Algorithm.CGLS, 10)))):
+            fn()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            loops[name] = time.perf_counter() - t0
+        out["config1_loops"] = {**loops, "api": "os_sart / cgls on host "
+                                "numpy, 64^3, 100 views (reference: SIRT "
+                                "15.13 s, CGLS 15.66 s, 8 cores)"}
+
         from oracle import oracle as O
         threads = O.default_threads()
         x_np = vol.cpu().numpy()

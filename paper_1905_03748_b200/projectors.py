@@ -113,6 +113,62 @@ def to_device(data, stream=None) -> torch.Tensor:
 _PINNED_MIN_BYTES = 1 << 20
 
 
+_DRAIN_VIEWS = 90  # views per chunk of an overlapped drain
+
+
+def _chunked_to_host(launch, out: torch.Tensor, a0: int, a1: int):
+    """Run launch(c0, c1) per view chunk on the current stream and copy each
+    finished chunk of ``out`` (rows a - a0) to one pinned host array on a
+    side stream, overlapping the device->host drain with the next chunk's
+    kernels.  Returns the host array (a numpy view of the pinned buffer)."""
+    cur = torch.cuda.current_stream(out.device)
+    side = _side_stream(out.device)
+    host = torch.empty(tuple(out.shape), dtype=torch.float32, pin_memory=True)
+    for c0 in range(a0, a1, _DRAIN_VIEWS):
+        c1 = min(a1, c0 + _DRAIN_VIEWS)
+        launch(c0, c1)
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        side.wait_event(ev)
+        with torch.cuda.stream(side):
+            host[c0 - a0:c1 - a0].copy_(out[c0 - a0:c1 - a0],
+                                        non_blocking=True)
+    out.record_stream(side)
+    side.synchronize()
+    return host.numpy()
+
+
+def _chunked_from_host(data: np.ndarray, device, launch, a0: int, a1: int):
+    """Upload host rows [a - a0] chunk by chunk on a side stream and run
+    launch(chunk_tensor, c0, c1) on the current stream as each arrives."""
+    cur = torch.cuda.current_stream(device)
+    side = _side_stream(device)
+    src = torch.from_numpy(np.ascontiguousarray(data, dtype=DTYPE))
+    dev = torch.empty(tuple(src.shape), dtype=torch.float32, device=device)
+    side.wait_stream(cur)  # dev's memory may be reused from cur's past work
+    for c0 in range(a0, a1, _DRAIN_VIEWS):
+        c1 = min(a1, c0 + _DRAIN_VIEWS)
+        with torch.cuda.stream(side):
+            dev[c0 - a0:c1 - a0].copy_(src[c0 - a0:c1 - a0],
+                                       non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(side)
+        cur.wait_event(ev)
+        launch(dev[c0 - a0:c1 - a0], c0, c1)
+    dev.record_stream(cur)
+    side.synchronize()  # the host source may be released after return
+
+
+_SIDE = {}
+
+
+def _side_stream(device) -> torch.cuda.Stream:
+    s = _SIDE.get(device)
+    if s is None:
+        s = _SIDE[device] = torch.cuda.Stream(device)
+    return s
+
+
 def to_host(t) -> np.ndarray:
     """Host numpy copy of a tensor.  Large device results drain through a
     page-locked buffer (torch's caching host allocator) at full PCIe rate;
@@ -293,12 +349,16 @@ def forward_project_slab(volume: Volume, geometry: ScanGeometry,
     if out is None:
         out = torch.empty((a1 - a0, det.n_v, det.n_u), dtype=torch.float32,
                           device=vol.device)
-    if method is ProjectionMethod.INTERPOLATED:
-        K.fwd_interp(vol, geometry, (a0, a1), volume.slab_range, out)
-    else:
-        K.fwd_siddon(vol, geometry, (a0, a1), volume.slab_range, out)
-    data = out if volume.on_device else to_host(out)
-    return ProjectionStack(det, data, (a0, a1))
+    fwd = K.fwd_interp if method is ProjectionMethod.INTERPOLATED \
+        else K.fwd_siddon
+    if volume.on_device:
+        fwd(vol, geometry, (a0, a1), volume.slab_range, out)
+        return ProjectionStack(det, out, (a0, a1))
+    # host caller: views in chunks, each chunk drained to pinned host memory
+    # on a side stream while the next one projects
+    return ProjectionStack(det, _chunked_to_host(
+        lambda c0, c1: fwd(vol, geometry, (c0, c1), volume.slab_range,
+                           out[c0 - a0:c1 - a0]), out, a0, a1), (a0, a1))
 
 
 def backproject_chunk_into(acc, projections: ProjectionStack,
@@ -312,15 +372,21 @@ def backproject_chunk_into(acc, projections: ProjectionStack,
     if not isinstance(mode, WeightMode):
         raise ValueError(f"unknown weight mode {mode}")
     a0, a1 = projections.angle_range
-    proj = to_device(projections.data)
     if isinstance(acc, torch.Tensor) and acc.is_cuda:
         dev_acc = acc
     else:
         dev_acc = to_device(np.asarray(acc, dtype=np.float32))
-    if mode is WeightMode.FDK:
-        K.bwd_fdk(proj, geometry, (a0, a1), slab_range, dev_acc)
+    bwd = K.bwd_fdk if mode is WeightMode.FDK else K.bwd_matched
+    if projections.on_device:
+        bwd(to_device(projections.data), geometry, (a0, a1), slab_range,
+            dev_acc)
     else:
-        K.bwd_matched(proj, geometry, (a0, a1), slab_range, dev_acc)
+        # host projections: view chunks uploaded on a side stream while the
+        # previous chunk backprojects (Atb is additive over views)
+        _chunked_from_host(
+            projections.data, dev_acc.device,
+            lambda p, c0, c1: bwd(p, geometry, (c0, c1), slab_range,
+                                  dev_acc), a0, a1)
     if dev_acc is not acc:
         acc[...] = to_host(dev_acc).astype(acc.dtype)
 
