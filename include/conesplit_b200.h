@@ -43,6 +43,9 @@ typedef void* cs_stream_t; /* cudaStream_t */
 /* Library identity / diagnostics. */
 const char* cs_version(void);
 const char* cs_last_error(void);
+/* Kernels launched by the library since it was loaded (diagnostics; the
+ * bench's gpu_launches claim). */
+long long cs_launch_count(void);
 /* Blocks the host until `stream` drains (the only synchronising call). */
 int cs_sync(cs_stream_t stream);
 

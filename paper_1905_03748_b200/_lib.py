@@ -38,6 +38,7 @@ SYMBOLS: dict[str, list] = {
     "cs_version": [],
     "cs_last_error": [],
     "cs_sync": [P],
+    "cs_launch_count": [],
     "cs_fwd_interp": [P, I, I, I, I, I, P, P, I, I, I, D, P, I, P],
     "cs_fwd_interp_residual": [P, I, I, I, P, P, I, I, I, D, P, P, P, P],
     "cs_fwd_siddon": [P, I, I, I, I, I, P, P, I, I, I, P, I, P],
@@ -73,7 +74,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         fn = getattr(L_, name)
         fn.argtypes = argtypes
         fn.restype = ctypes.c_char_p if name in (
-            "cs_version", "cs_last_error") else ctypes.c_int
+            "cs_version", "cs_last_error") else (
+            ctypes.c_longlong if name == "cs_launch_count" else ctypes.c_int)
     return L_
 
 

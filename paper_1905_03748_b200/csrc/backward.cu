@@ -346,6 +346,7 @@ int cs_bwd_fdk(float* vol_acc, int nx, int ny, int z_lo, int n_slab,
         proj, dcs, n_a, grid6[0], grid6[1], grid6[2], grid6[3], grid6[4],
         grid6[5], nx, ny, z_lo, n_slab, dso, dsd, 1.0 / du, 1.0 / dv, off_u,
         off_v, n_u, n_v, vol_acc);
+    CS_COUNT_LAUNCH();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
       set_error("bwd_fdk launch: %s", cudaGetErrorString(e));
@@ -370,6 +371,7 @@ int cs_bwd_fdk(float* vol_acc, int nx, int ny, int z_lo, int n_slab,
         t->tex, dcs + a0, na, grid6[0], grid6[1], grid6[2], grid6[3],
         grid6[4], grid6[5], nx, ny, z_lo, n_slab, dso, dsd, 1.0 / du,
         1.0 / dv, off_u, off_v, n_u, n_v, vol_acc);
+    CS_COUNT_LAUNCH();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
       set_error("bwd_fdk launch: %s", cudaGetErrorString(e));
@@ -393,6 +395,7 @@ int cs_ray_table(int nx, int ny, int nz, const double* grid6,
   if (rc) return rc;
   ray_table_kernel<<<dim3((n_u + 127) / 128, n_v, n_a), 128, 0, s>>>(
       dgeom, G, step_max, n_u, n_v, t0, step, n);
+  CS_COUNT_LAUNCH();
   cudaError_t e = cudaGetLastError();
   release_geometry(dgeom, s);
   CS_CHECK_CUDA(e);

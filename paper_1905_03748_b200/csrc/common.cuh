@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <atomic>
 #include <stdint.h>
 #include <cstdio>
 #include <string>
@@ -16,6 +17,10 @@
 namespace cs {
 
 void set_error(const char* fmt, ...);
+
+// Kernels launched by this library since load (cs_launch_count()).
+extern std::atomic<long long> g_launches;
+#define CS_COUNT_LAUNCH() ::cs::g_launches.fetch_add(1, std::memory_order_relaxed)
 
 #define CS_CHECK_CUDA(expr)                                                  \
   do {                                                                       \

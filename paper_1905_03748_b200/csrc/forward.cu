@@ -235,6 +235,7 @@ static int launch_interp(const float* vol, int nx, int ny, int nz, int z_lo,
     kern<<<grid, block, 0, s>>>(t->tex, dgeom, G, step_max, s0, s1, n_u, n_v,
                                 v0, v1, out, first ? b : nullptr,
                                 first ? w : nullptr);
+    CS_COUNT_LAUNCH();
     CS_CHECK_CUDA(cudaGetLastError());
   }
   release_geometry(dgeom, s);
@@ -296,6 +297,7 @@ int cs_fwd_siddon(const float* vol, int nx, int ny, int nz, int z_lo,
                     (v1 - v0 + FWD_TILE_V - 1) / FWD_TILE_V, n_a);
     fwd_siddon_kernel<<<grid, 128, 0, s>>>(vol, dgeom, G, z_lo, z_hi, n_u,
                                            n_v, v0, v1, out, accumulate);
+    CS_COUNT_LAUNCH();
     e = cudaGetLastError();
   }
   release_geometry(dgeom, s);

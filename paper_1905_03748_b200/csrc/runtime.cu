@@ -1,5 +1,6 @@
 // runtime.cu -- error state, texture cache and geometry upload for the
 // conesplit B200 C-ABI.
+#include <atomic>
 #include <cstdarg>
 #include <cstdlib>
 #include <map>
@@ -11,6 +12,7 @@
 namespace cs {
 
 static thread_local char g_err[1024] = "";
+std::atomic<long long> g_launches{0};
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -235,6 +237,8 @@ extern "C" {
 const char* cs_version(void) { return "conesplit-b200 0.1.0 sm_100a"; }
 
 const char* cs_last_error(void) { return cs::g_err; }
+
+long long cs_launch_count(void) { return cs::g_launches.load(); }
 
 int cs_sync(cs_stream_t stream) {
   CS_CHECK_CUDA(cudaStreamSynchronize((cudaStream_t)stream));

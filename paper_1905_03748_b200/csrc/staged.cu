@@ -605,14 +605,18 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
                          200 * 1024);
     attr_set = true;
   }
-  if (nxm > 0 && rows(0) > 0)
+  if (nxm > 0 && rows(0) > 0) {
     k0<<<dim3(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids, G, step_max, z_lo, z_hi, n_u, n_v,
         band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_ok);
-  if (nall > nxm && rows(1) > 0)
+    CS_COUNT_LAUNCH();
+  }
+  if (nall > nxm && rows(1) > 0) {
     k1<<<dim3(gx, rows(1), nall - nxm), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids + nxm, G, step_max, z_lo, z_hi, n_u, n_v,
         band[1][0], band[1][1], out, proj_in, rb, rw, cap, budget, vec_ok);
+    CS_COUNT_LAUNCH();
+  }
   e = cudaGetLastError();
   cudaFreeAsync(ids, s);
   release_geometry(dgeom, s);

@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(1024)
 int reduce_into(const double* partial, size_t n, double* out,
                 cudaStream_t s) {
   reduce_partials_kernel<<<1, 1024, 0, s>>>(partial, n, out);
+  CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   return CS_OK;
 }
@@ -334,6 +335,7 @@ int cs_tv_grad_sumsq(const float* u, int nx, int ny, int nzw, int core_lo,
   CS_CHECK_CUDA(cudaMallocAsync((void**)&part, nb * sizeof(double), s));
   tv_gd_tiled_kernel<0><<<grid, dim3(TV_TX, TV_TY), 0, s>>>(
       u, nullptr, Win{nx, ny, nzw}, core_lo, core_hi, 0.0, nullptr, 1.0, part);
+  CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   rc = reduce_into(part, nb, out_sum, s);
   cudaFreeAsync(part, s);
@@ -351,6 +353,7 @@ int cs_tv_step(const float* u, float* u_out, int nx, int ny, int nzw,
   tv_gd_tiled_kernel<1><<<grid, dim3(TV_TX, TV_TY), 0, (cudaStream_t)stream>>>(
       u, u_out, Win{nx, ny, nzw}, 0, nzw, step, norm_sumsq_dev, scale,
       nullptr);
+  CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   return CS_OK;
 }
@@ -364,6 +367,7 @@ int cs_rof_iter(const float* f, const float* p_in, float* p_out, int nx,
   const dim3 grid((nx + 31) / 32, (ny + 7) / 8, nzw);
   rof_iter_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(
       f, p_in, p_out, Win{nx, ny, nzw}, (float)lam, (float)(ROF_TAU / lam));
+  CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   return CS_OK;
 }
@@ -375,6 +379,7 @@ int cs_rof_finish(const float* f, const float* p, float* u, int nx, int ny,
   const dim3 grid((nx + 31) / 32, (ny + 7) / 8, nzw);
   rof_finish_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(
       f, p, u, Win{nx, ny, nzw}, (float)lam);
+  CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   return CS_OK;
 }
@@ -390,6 +395,7 @@ int cs_tv_norm(const float* u, int nx, int ny, int nzw, double* out_sum,
   retain_pool();
   CS_CHECK_CUDA(cudaMallocAsync((void**)&part, nb * sizeof(double), s));
   tv_norm_kernel<<<grid, dim3(32, 8), 0, s>>>(u, Win{nx, ny, nzw}, part);
+  CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   rc = reduce_into(part, nb, out_sum, s);
   cudaFreeAsync(part, s);

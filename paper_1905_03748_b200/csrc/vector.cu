@@ -118,6 +118,7 @@ int cs_dot(const float* a, const float* b, int64_t n, double* out_sum,
   double* part = nullptr;
   CS_CHECK_CUDA(cudaMallocAsync((void**)&part, nb * sizeof(double), s));
   dot_kernel<<<nb, 256, 0, s>>>(a, b, n, part);
+  CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   int rc = reduce_into(part, nb, out_sum, s);
   cudaFreeAsync(part, s);
@@ -129,6 +130,7 @@ int cs_axpy_ratio(float* y, const float* x, int64_t n, const double* num,
   if (n <= 0) return CS_OK;
   axpy_ratio_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
       y, x, n, num, den, sign);
+  CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   return CS_OK;
 }
@@ -138,6 +140,7 @@ int cs_xpay_ratio(float* p, const float* s, int64_t n, const double* num,
   if (n <= 0) return CS_OK;
   xpay_ratio_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(p, s, n,
                                                                    num, den);
+  CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   return CS_OK;
 }
@@ -147,6 +150,7 @@ int cs_guarded_inverse(const float* a, float* out, int64_t n,
   if (n <= 0) return CS_OK;
   guarded_inverse_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
       a, out, n);
+  CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   return CS_OK;
 }
@@ -156,6 +160,7 @@ int cs_sart_update(float* x, float* upd, const float* v, double lam,
   if (n <= 0) return CS_OK;
   sart_update_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
       x, upd, v, (float)lam, n);
+  CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   return CS_OK;
 }
@@ -163,6 +168,7 @@ int cs_sart_update(float* x, float* upd, const float* v, double lam,
 int cs_fill(float* x, float value, int64_t n, cs_stream_t stream) {
   if (n <= 0) return CS_OK;
   fill_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(x, value, n);
+  CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   return CS_OK;
 }

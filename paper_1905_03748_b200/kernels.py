@@ -17,6 +17,11 @@ from .geometry import ScanGeometry, VoxelGrid, flat_geometry, grid6
 MAX_ANGLES_PER_LAUNCH = 65535  # grid.z limit of the ray kernels
 
 
+def launch_count() -> int:
+    """Kernels the library has launched since it was loaded."""
+    return int(lib().cs_launch_count())
+
+
 def _f32(t: torch.Tensor, name: str) -> torch.Tensor:
     if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
         raise ValueError(f"{name} must be a contiguous float32 CUDA tensor")
