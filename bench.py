@@ -453,12 +453,21 @@ def run_extras(args, cs, K, g, vol, y, dev, rank, world, arange, zrange):
         torch.cuda.synchronize()
         iters.append((time.perf_counter() - t1) * 1e3)
     dt = (time.perf_counter() - t0) / ne
-    upd = float(a1 - a0) * n ** 3 + float(A) * (z1 - z0) * n * n
+    if world > 1:
+        # whole-job aggregate: every rank does equal work; slowest rank
+        import torch.distributed as dist
+        on_dev = os.environ.get("CS_BENCH_BACKEND", "nccl") == "nccl"
+        tt = torch.tensor([dt], dtype=torch.float64,
+                          device=dev if on_dev else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+    upd = (float(a1 - a0) * n ** 3 + float(A) * (z1 - z0) * n * n) * world
     out["e2e"] = {"value": upd / dt / 1e9, "unit": "GUPS",
                   "h2d_bytes_per_step": int(vol_np.nbytes + y_np.nbytes),
                   "d2h_bytes_per_step": int(p.data.nbytes + v.data.nbytes),
                   "ms_per_step": dt * 1e3,
                   "iter_ms": [round(x, 1) for x in iters],
+                  "scope": f"all {world} rank(s); slowest rank's time",
                   "api": "forward_project_slab + backproject_slab(MATCHED)"
                          " on host numpy (pinned)"}
     del vol_h, y_h
