@@ -241,6 +241,22 @@ __device__ __forceinline__ float divp(const float* __restrict__ p,
   return d;
 }
 
+// div p at the voxel whose three components sit at pz[0], pz[vol],
+// pz[2 vol] (pointer already offset to the voxel): same terms and order as
+// divp, 32-bit neighbour strides (plane = nx ny < 2^31).
+__device__ __forceinline__ float divp_at(const float* __restrict__ pzi,
+                                         size_t vol, int plane, int nx,
+                                         bool zl, bool zf, bool yl, bool yf,
+                                         bool xl, bool xf) {
+  const float* pyi = pzi + vol;
+  const float* pxi = pyi + vol;
+  float d = 0.f;
+  d += (zl ? __ldg(pzi) : 0.f) - (zf ? __ldg(pzi - plane) : 0.f);
+  d += (yl ? __ldg(pyi) : 0.f) - (yf ? __ldg(pyi - nx) : 0.f);
+  d += (xl ? __ldg(pxi) : 0.f) - (xf ? __ldg(pxi - 1) : 0.f);
+  return d;
+}
+
 __global__ void __launch_bounds__(256)
     rof_iter_kernel(const float* __restrict__ f, const float* __restrict__ pin,
                     float* __restrict__ pout, Win W, float lam,
@@ -249,24 +265,39 @@ __global__ void __launch_bounds__(256)
   const int y = blockIdx.y * 8 + threadIdx.y;
   const int z = blockIdx.z;
   if (x >= W.nx || y >= W.ny) return;
-  const size_t vol = (size_t)W.nx * W.ny * W.nz;
-  const size_t i = W.at(x, y, z);
+  const int nx = W.nx, plane = W.nx * W.ny;
+  const size_t vol = (size_t)plane * W.nz;
+  const size_t i = (size_t)z * plane + (size_t)(y * nx + x);
+  const float* fi = f + i;
+  const float* pi = pin + i;
+  // "l": the forward difference exists (not the last plane/row/column);
+  // "f": the backward one exists (not the first)
+  const bool zl = z < W.nz - 1, zf = z > 0, yl = y < W.ny - 1, yf = y > 0;
+  const bool xl = x < nx - 1, xf = x > 0;
   // u = f + lam div p at i and at the +1 neighbours (forward gradient)
-  const float uc = __ldg(f + i) + lam * divp(pin, W, vol, x, y, z);
+  const float uc = __ldg(fi) + lam * divp_at(pi, vol, plane, nx, zl, zf, yl,
+                                             yf, xl, xf);
   float gz = 0.f, gy = 0.f, gx = 0.f;
-  if (z < W.nz - 1)
-    gz = (__ldg(f + W.at(x, y, z + 1)) + lam * divp(pin, W, vol, x, y, z + 1)) - uc;
-  if (y < W.ny - 1)
-    gy = (__ldg(f + W.at(x, y + 1, z)) + lam * divp(pin, W, vol, x, y + 1, z)) - uc;
-  if (x < W.nx - 1)
-    gx = (__ldg(f + W.at(x + 1, y, z)) + lam * divp(pin, W, vol, x + 1, y, z)) - uc;
-  float qz = __ldg(pin + i) + tau_over_lam * gz;
-  float qy = __ldg(pin + vol + i) + tau_over_lam * gy;
-  float qx = __ldg(pin + 2 * vol + i) + tau_over_lam * gx;
+  if (zl)
+    gz = (__ldg(fi + plane) +
+          lam * divp_at(pi + plane, vol, plane, nx, z + 1 < W.nz - 1, true,
+                        yl, yf, xl, xf)) - uc;
+  if (yl)
+    gy = (__ldg(fi + nx) +
+          lam * divp_at(pi + nx, vol, plane, nx, zl, zf, y + 1 < W.ny - 1,
+                        true, xl, xf)) - uc;
+  if (xl)
+    gx = (__ldg(fi + 1) +
+          lam * divp_at(pi + 1, vol, plane, nx, zl, zf, yl, yf,
+                        x + 1 < nx - 1, true)) - uc;
+  float qz = __ldg(pi) + tau_over_lam * gz;
+  float qy = __ldg(pi + vol) + tau_over_lam * gy;
+  float qx = __ldg(pi + 2 * vol) + tau_over_lam * gx;
   const float mag = fmaxf(sqrtf(qz * qz + qy * qy + qx * qx), 1.f);
-  pout[i] = qz / mag;
-  pout[vol + i] = qy / mag;
-  pout[2 * vol + i] = qx / mag;
+  float* po = pout + i;
+  po[0] = qz / mag;
+  po[vol] = qy / mag;
+  po[2 * vol] = qx / mag;
 }
 
 __global__ void __launch_bounds__(256)

@@ -160,5 +160,11 @@ def test_fullsize_crop_vs_oracle(n, crop):
     refb = O.bwd_matched(y, og, (0, 2), zr)
     assert float(np.abs(refb).sum()) > 0.0
     e_b = rel_l2(acc.cpu(), refb)
-    print(f"n={n}: Ax relL2 {e_ax:.3e}, matched relL2 {e_b:.3e}")
-    assert e_ax <= 1e-5 and e_b <= 1e-5, (e_ax, e_b)
+    # FDK-weighted Atb of the same crop into the same slab
+    acc.zero_()
+    K.bwd_fdk(torch.from_numpy(y).cuda(), g, (0, 2), zr, acc)
+    reff = O.bwd_fdk(y, og, (0, 2), zr)
+    e_f = rel_l2(acc.cpu(), reff)
+    print(f"n={n}: Ax relL2 {e_ax:.3e}, matched relL2 {e_b:.3e}, "
+          f"FDK relL2 {e_f:.3e}")
+    assert e_ax <= 1e-5 and e_b <= 1e-5 and e_f <= 1e-5, (e_ax, e_b, e_f)
