@@ -29,7 +29,7 @@ METRICS = [
     ("launch__registers_per_thread", "regs"),
     ("smsp__inst_executed.sum", "warp insts"),
 ]
-KEYS = {"fwd_interp": "fwd_interp_kernel", "bwd_matched": "bwd_matched_kernel",
+KEYS = {"fwd_interp": "fwd_interp_kernel",
         "staged_kernel<1": "bwd_matched_kernel",
         "bwd_fdk": "bwd_fdk_kernel", "fdk_staged": "bwd_fdk_kernel",
         "fwd_siddon": "fwd_siddon_kernel"}

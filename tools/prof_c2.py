@@ -38,5 +38,7 @@ for rep in range(2):
         K.bwd_matched(y[0:C], g, (0, C), (0, n), acc)
     if "fdk" in which:
         K.bwd_fdk(y[0:C], g, (0, C), (0, n), acc)
+    if "siddon" in which:
+        K.fwd_siddon(vol, g, (0, C), (0, n), proj)
 torch.cuda.synchronize()
 print("done")
