@@ -597,13 +597,18 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   };
   auto k0 = staged_kernel<OP, 0, MODE>;
   auto k1 = staged_kernel<OP, 1, MODE>;
-  static bool attr_set = false;  // per process; one device per ordinal
-  if (!attr_set) {
+  // the dynamic shared-memory opt-in is per device: set it once on each
+  // (the executor drives several GPUs from one process)
+  static std::atomic<unsigned long long> attr_done{0};
+  int dev_ord = 0;
+  cudaGetDevice(&dev_ord);
+  const unsigned long long bit = 1ull << (dev_ord & 63);
+  if (!(attr_done.load() & bit)) {
     cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    attr_set = true;
+    attr_done.fetch_or(bit);
   }
   if (nxm > 0 && rows(0) > 0) {
     k0<<<dim3(gx, rows(0), nxm), ST_THREADS, smem, s>>>(

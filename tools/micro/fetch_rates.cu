@@ -91,6 +91,17 @@ __global__ void __launch_bounds__(256) k(cudaTextureObject_t tex,
           const float* q = gv + ((size_t)(layer0 + 1) * 256 + yi) * 512 + (xi & 511);
           acc += __ldg(q) + __ldg(q + 1) + __ldg(q + 512) + __ldg(q + 513);
         }
+      } else if (MODE == 13) {  // Ax-like: 8u x 4v rays, lanes 1.41 texels apart
+        const float xr = (float)((blockIdx.x & 7) * 48) + (float)(lane & 7) * 1.41f + f + (float)j * 0.5f;
+        const float yr = (float)(((blockIdx.x >> 3) & 7) * 24) + (float)(lane >> 3) * 1.41f + f * 0.3f;
+        float4 r = g4(tex, layer0 + (j & 1), xr, yr);
+        acc += r.x + r.y + r.z + r.w;
+      } else if (MODE == 14) {  // quad = 4 consecutive samples (0.5 texel) of one ray
+        const int ray = lane >> 2, smp = lane & 3;
+        const float xr = (float)((blockIdx.x & 7) * 48) + (float)(ray & 7) * 1.41f + f + (float)(j * 4 + smp) * 0.5f;
+        const float yr = (float)(((blockIdx.x >> 3) & 7) * 24) + (float)(warp & 3) * 1.41f + f * 0.3f;
+        float4 r = g4(tex, layer0 + (j & 1), xr, yr);
+        acc += r.x + r.y + r.z + r.w;
       } else if (MODE == 12) {  // 2 float4 point fetches (one sample's 8 taps)
         float4 r = tex2DLayered<float4>(tex4, x, y, layer0 + (j & 1));
         float4 r2 = tex2DLayered<float4>(tex4, x, y + 1.f, layer0 + (j & 1));
@@ -159,12 +170,12 @@ int main() {
   const int blocks = sms * 8, iters = 4000;
   const char* names[] = {"tld4 (4 val)", "tex point (1 val)", "lds32", "lds64",
                          "lds128", "ldg32 L1-hit", "ldg64 L1-hit",
-                         "mix tld4 + 4 lds32", "tex float4 point", "tex float2 point", "ldg32 scattered 8y4z", "mix tld4 + 4 ldg32", "2x float4 point (8 taps)"};
+                         "mix tld4 + 4 lds32", "tex float4 point", "tex float2 point", "ldg32 scattered 8y4z", "mix tld4 + 4 ldg32", "2x float4 point (8 taps)", "tld4 Ax-like spread rays", "tld4 quad = 4 samples of a ray"};
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   printf("SMs %d, clock %.3f GHz (nominal max)\n", sms, ghz);
-  for (int mode = 0; mode < 13; mode++) {
+  for (int mode = 0; mode < 15; mode++) {
     for (int rep = 0; rep < 2; rep++) {
       cudaEventRecord(a);
       switch (mode) {
@@ -181,6 +192,8 @@ int main() {
         case 10: k<10><<<blocks, 256>>>(tex, tex4, tex2, gv, g, out, iters); break;
         case 11: k<11><<<blocks, 256>>>(tex, tex4, tex2, gv, g, out, iters); break;
         case 12: k<12><<<blocks, 256>>>(tex, tex4, tex2, gv, g, out, iters); break;
+        case 13: k<13><<<blocks, 256>>>(tex, tex4, tex2, gv, g, out, iters); break;
+        case 14: k<14><<<blocks, 256>>>(tex, tex4, tex2, gv, g, out, iters); break;
       }
       cudaEventRecord(b);
       cudaEventSynchronize(b);
