@@ -102,6 +102,21 @@ __global__ void __launch_bounds__(256) k(cudaTextureObject_t tex,
         const float yr = (float)(((blockIdx.x >> 3) & 7) * 24) + (float)(warp & 3) * 1.41f + f * 0.3f;
         float4 r = g4(tex, layer0 + (j & 1), xr, yr);
         acc += r.x + r.y + r.z + r.w;
+      } else if (MODE == 15) {  // 25% of lanes active, one per quad
+        if (((lane + j) & 3) == 0) {
+          float4 r = g4(tex, layer0 + (j & 1), x, y);
+          acc += r.x + r.y + r.z + r.w;
+        }
+      } else if (MODE == 16) {  // 25% of lanes active, whole quads
+        if ((((lane >> 2) + j) & 3) == 0) {
+          float4 r = g4(tex, layer0 + (j & 1), x, y);
+          acc += r.x + r.y + r.z + r.w;
+        }
+      } else if (MODE == 17) {  // 25% of lanes active, one warp-quarter (8 lanes)
+        if ((((lane >> 3) + j) & 3) == 0) {
+          float4 r = g4(tex, layer0 + (j & 1), x, y);
+          acc += r.x + r.y + r.z + r.w;
+        }
       } else if (MODE == 12) {  // 2 float4 point fetches (one sample's 8 taps)
         float4 r = tex2DLayered<float4>(tex4, x, y, layer0 + (j & 1));
         float4 r2 = tex2DLayered<float4>(tex4, x, y + 1.f, layer0 + (j & 1));
@@ -170,12 +185,12 @@ int main() {
   const int blocks = sms * 8, iters = 4000;
   const char* names[] = {"tld4 (4 val)", "tex point (1 val)", "lds32", "lds64",
                          "lds128", "ldg32 L1-hit", "ldg64 L1-hit",
-                         "mix tld4 + 4 lds32", "tex float4 point", "tex float2 point", "ldg32 scattered 8y4z", "mix tld4 + 4 ldg32", "2x float4 point (8 taps)", "tld4 Ax-like spread rays", "tld4 quad = 4 samples of a ray"};
+                         "mix tld4 + 4 lds32", "tex float4 point", "tex float2 point", "ldg32 scattered 8y4z", "mix tld4 + 4 ldg32", "2x float4 point (8 taps)", "tld4 Ax-like spread rays", "tld4 quad = 4 samples of a ray", "tld4 25% lanes (1/quad)", "tld4 25% lanes (whole quads)", "tld4 25% lanes (8 contiguous)"};
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   printf("SMs %d, clock %.3f GHz (nominal max)\n", sms, ghz);
-  for (int mode = 0; mode < 15; mode++) {
+  for (int mode = 0; mode < 18; mode++) {
     for (int rep = 0; rep < 2; rep++) {
       cudaEventRecord(a);
       switch (mode) {
@@ -194,6 +209,9 @@ int main() {
         case 12: k<12><<<blocks, 256>>>(tex, tex4, tex2, gv, g, out, iters); break;
         case 13: k<13><<<blocks, 256>>>(tex, tex4, tex2, gv, g, out, iters); break;
         case 14: k<14><<<blocks, 256>>>(tex, tex4, tex2, gv, g, out, iters); break;
+        case 15: k<15><<<blocks, 256>>>(tex, tex4, tex2, gv, g, out, iters); break;
+        case 16: k<16><<<blocks, 256>>>(tex, tex4, tex2, gv, g, out, iters); break;
+        case 17: k<17><<<blocks, 256>>>(tex, tex4, tex2, gv, g, out, iters); break;
       }
       cudaEventRecord(b);
       cudaEventSynchronize(b);
