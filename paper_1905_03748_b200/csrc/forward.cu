@@ -144,6 +144,12 @@ __global__ void __launch_bounds__(128)
       }
     }
     const size_t plane = (size_t)nx * ny;
+    // The voxel of a piece is floor of its midpoint / voxel size
+    // (_kernels.py:71-151).  A midpoint lies mid-voxel (>= half the piece,
+    // > 5e-13, from any plane), so multiplying by the fp64 reciprocal picks
+    // the same voxel as the division -- three fp64 divisions per piece were
+    // the kernel's largest cost.
+    const double ivx = 1.0 / vx, ivy = 1.0 / vy, ivz = 1.0 / vz;
     double t = t0;
     while (t < t1 - 1e-12) {
       double tnext = fmin(fmin(tn[0], tn[1]), tn[2]);
@@ -151,9 +157,9 @@ __global__ void __launch_bounds__(128)
       const double seg = tnext - t;
       if (seg > 1e-12) {
         const double tm = 0.5 * (t + tnext);
-        const int ix = (int)floor((o[0] + tm * d[0] - gx0) / vx);
-        const int iy = (int)floor((o[1] + tm * d[1] - gy0) / vy);
-        const int iz = (int)floor((o[2] + tm * d[2] - gz0) / vz);
+        const int ix = (int)floor((o[0] + tm * d[0] - gx0) * ivx);
+        const int iy = (int)floor((o[1] + tm * d[1] - gy0) * ivy);
+        const int iz = (int)floor((o[2] + tm * d[2] - gz0) * ivz);
         if (ix >= 0 && ix < nx && iy >= 0 && iy < ny && iz >= z_lo &&
             iz < z_hi)
           acc += seg * (double)__ldg(vol + (size_t)(iz - z_lo) * plane +
