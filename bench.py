@@ -487,6 +487,24 @@ def run_extras(args, cs, K, g, vol, y, dev, rank, world, arange, zrange):
             ts[iters] = time.perf_counter() - t0
         out["os_sart_s_per_iter"] = (ts[3] - ts[1]) / 2
         out["os_sart_setup_plus_1iter_s"] = ts[1]
+        # SART-TV (SURVEY 8(d) C4 loop form: TV-GD 20 inner iterations,
+        # ExactGlobal norm, after every OS-SART iteration) and the FDK
+        # pipeline (cosine weight, ramp filter, FDK Atb) at config 2
+        tv = cs.TvParams(cs.TvMinimizer.GRADIENT_DESCENT, 1, 20, 1e-3)
+        for iters in (1, 1, 2):
+            cfg = cs.ReconConfig(pool, cs.Algorithm.OSSART, iters, 36, tv=tv)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            cs.os_sart(b, g, cfg)
+            torch.cuda.synchronize()
+            ts[iters] = time.perf_counter() - t0
+        out["sart_tv_s_per_iter"] = ts[2] - ts[1]
+        cs.fdk(b, g, pool)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cs.fdk(b, g, pool)
+        torch.cuda.synchronize()
+        out["fdk_s"] = time.perf_counter() - t0
 
         # Config 1 loops end to end through the public API (host numpy in,
         # host numpy out), the reference's own timing case (BASELINE.md
