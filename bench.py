@@ -170,6 +170,16 @@ def load_traffic(kernel_key):
         return None
 
 
+def load_limits(kernel_key):
+    """ncu pipe utilisations of a kernel from the committed summary
+    (profiles/ncu_limits.json), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_limits.json")))
+        return d.get(kernel_key)
+    except (OSError, ValueError):
+        return None
+
+
 def measured_peak():
     try:
         d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -350,7 +360,10 @@ def run_ours(args):
                      "peak_source": peak_kind,
                      "bytes_per_update": bpu,
                      "updates_per_launch": kupd,
-                     "launch_ms": kt * 1e3},
+                     "launch_ms": kt * 1e3,
+                     # the pipe that actually bounds this gather kernel
+                     # (ncu --set full, committed summary)
+                     "ncu_pipes": load_limits(kname)},
         "clocks": clocks,
         "gpu_launches": launches,
     }

@@ -75,6 +75,32 @@ def main():
                         # matched = x-major + y-major views): sum them
                         sums[key] = sums.get(key, 0.0) + rd + wr
     traffic.update(sums)
+    # pipe limiters per kernel key (bench.py reports them beside the HBM
+    # roofline of the dominant kernel)
+    lim_path = os.path.join(ROOT, "profiles", "ncu_limits.json")
+    try:
+        limits = json.load(open(lim_path))
+    except (OSError, ValueError):
+        limits = {}
+    for rec in rows_out:
+        for k, key in KEYS.items():
+            if k not in rec["kernel"]:
+                continue
+            ent = {}
+            for label in ("TEX writeback %", "issue active %", "L1/TEX thru %",
+                          "dram %"):
+                if label in rec:
+                    try:
+                        v = float(rec[label][0])
+                    except ValueError:
+                        continue
+                    if v == v:
+                        ent[label] = v
+            if ent:
+                ent["report"] = f"profiles/ncu_{tag}.md"
+                limits[key] = ent
+    with open(lim_path, "w") as f:
+        json.dump(limits, f, indent=1)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     md = [f"# ncu --set full summary ({tag})", "",
           "Captured with `ncu --set full --clock-control none --import-source on`"
