@@ -266,6 +266,31 @@ def _upload(dst: torch.Tensor, src, stream, link: "_HostLink | None"):
         dst.copy_(src, non_blocking=True)
 
 
+def _refine_for_overlap(slabs, plane: int, fixed_bytes: int, budget: int,
+                        max_factor: int = 4):
+    """The plan's slabs are the fewest that fit one slab beside the other
+    buffers (scheduler.py:169-210); with one slab buffer the upload of slab
+    s+1 cannot overlap slab s's kernels.  Split every slab into the
+    smallest number of equal parts (<= max_factor) for which two slab
+    buffers fit beside ``fixed_bytes``, so transfers double-buffer.  (Slab
+    results concatenate / add up exactly as the plan's -- Atb is
+    slab-partition invariant, Ax partials differ by fp32 rounding only.)"""
+    if len(slabs) < 2:
+        return slabs
+    longest = max(z1 - z0 for z0, z1 in slabs)
+    if fixed_bytes + 2 * longest * plane * SCALAR_BYTES <= budget:
+        return slabs
+    for r in range(2, max_factor + 1):
+        part = -(-longest // r)
+        if fixed_bytes + 2 * part * plane * SCALAR_BYTES <= budget:
+            out = []
+            for z0, z1 in slabs:
+                step = -(-(z1 - z0) // r)
+                out.extend((z, min(z + step, z1)) for z in range(z0, z1, step))
+            return tuple(out)
+    return slabs
+
+
 def _join_streams(dev: _Device):
     """Order the caller's stream after the worker streams, so buffers the
     caching allocator hands back (allocated on the current stream) are not
@@ -412,11 +437,12 @@ def execute_forward(volume: Volume, geometry: ScanGeometry, pool: DevicePool,
                 parts[i] = acc
                 _join_streams(dev)
                 return
-            slabs = plan.slab_ranges
+            window = (a1 - a0) * sheet * SCALAR_BYTES
+            slabs = _refine_for_overlap(plan.slab_ranges, plane, window,
+                                        dev.budget)
             longest = max(z1 - z0 for z0, z1 in slabs)
             nbuf = 1 if len(slabs) == 1 else 2
             staging = _HostLink() if isinstance(src, np.ndarray) else None
-            window = (a1 - a0) * sheet * SCALAR_BYTES
             slab_bytes = longest * plane * SCALAR_BYTES
             if window + nbuf * slab_bytes <= dev.budget:
                 parts[i] = _forward_resident(dev, src, slabs, nbuf, longest,
@@ -616,10 +642,22 @@ def execute_backward(projections: ProjectionStack, geometry: ScanGeometry,
         devs[i] = dev
         with torch.cuda.device(dev.cuda):
             src = projections.data
-            longest = max(slabs[q][1] - slabs[q][0] for q in queues[i])
-            nbuf = 1 if len(queues[i]) == 1 else 2
-            slab_bytes = longest * plane * SCALAR_BYTES
             local = on_dev and src.device == dev.cuda
+            # this device's slabs, refined for double buffering when the
+            # budget only holds one slab beside the projections (uploaded
+            # once when they fit, else streamed in plan chunks)
+            C0 = min(plan.chunk_angles, A)
+            mine = tuple(slabs[q] for q in queues[i])
+            proj_bytes = 0 if local else A * sheet * SCALAR_BYTES
+            cand = _refine_for_overlap(mine, plane, proj_bytes, dev.budget)
+            if proj_bytes + 2 * max(z1 - z0 for z0, z1 in cand) * plane * \
+                    SCALAR_BYTES > dev.budget and len(cand) > 1:
+                cand = _refine_for_overlap(
+                    mine, plane, 2 * C0 * sheet * SCALAR_BYTES, dev.budget)
+            mine = list(cand)
+            longest = max(z1 - z0 for z0, z1 in mine)
+            nbuf = 1 if len(mine) == 1 else 2
+            slab_bytes = longest * plane * SCALAR_BYTES
             whole = local or (A * sheet * SCALAR_BYTES + nbuf * slab_bytes
                               <= dev.budget)
             if not whole and nbuf * slab_bytes + 2 * min(
@@ -664,8 +702,8 @@ def execute_backward(projections: ProjectionStack, geometry: ScanGeometry,
                 de.record(dev.d2h)
                 drained[b_] = de
 
-            for qi, si in enumerate(queues[i]):
-                z0, z1 = slabs[si]
+            for qi, (z0, z1) in enumerate(mine):
+                si = qi
                 b = qi % nbuf
                 if waiting is not None and waiting[0] == b:
                     drain(waiting)   # single buffer: drain before reuse
