@@ -197,3 +197,27 @@ def test_halo_slabs_match_reference():
                 for s in cs.regularization.make_halo_slabs(nz, n, d)]
         ref = O.make_halo_slabs(nz, n, d)
         assert ours == ref
+
+
+def test_refine_for_overlap():
+    """Executor slab refinement (execution._refine_for_overlap): the fewest
+    equal parts (<= 4) letting two slab buffers fit beside fixed bytes;
+    parts tile every slab exactly and keep the plan's order."""
+    from paper_1905_03748_b200.execution import _refine_for_overlap
+    plane = 1000  # elements per plane -> 4000 B
+    slabs = ((0, 10), (10, 20), (20, 25))
+    # two 10-plane buffers fit: unchanged
+    assert _refine_for_overlap(slabs, plane, 1000, 2 * 10 * 4000 + 1000) == slabs
+    # only 2 x 5 planes fit: halves
+    out = _refine_for_overlap(slabs, plane, 0, 2 * 5 * 4000)
+    assert out == ((0, 5), (5, 10), (10, 15), (15, 20), (20, 23), (23, 25))
+    # nothing up to 4 parts fits: unchanged (the chunked path takes over)
+    assert _refine_for_overlap(slabs, plane, 0, 2 * 2 * 4000) == slabs
+    # a single slab is left alone
+    assert _refine_for_overlap(((0, 7),), plane, 0, 10) == ((0, 7),)
+    for budget in range(40000, 200000, 7000):
+        out = _refine_for_overlap(slabs, plane, 3000, budget)
+        flat = [z for s in out for z in s]
+        assert flat[0] == 0 and flat[-1] == 25
+        assert all(a[1] == b[0] for a, b in zip(out, out[1:]))
+        assert all(b > a for a, b in out)
