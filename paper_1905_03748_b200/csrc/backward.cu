@@ -20,7 +20,10 @@
 
 namespace cs {
 
-constexpr int FDK_ZB = 16;  // z voxels per thread (registers)
+#ifndef CS_FDK_ZB
+#define CS_FDK_ZB 16
+#endif
+constexpr int FDK_ZB = CS_FDK_ZB;  // z voxels per thread (registers)
 
 __global__ void __launch_bounds__(128)
     bwd_fdk_kernel(cudaTextureObject_t tex, const double2* __restrict__ cs,
@@ -89,7 +92,10 @@ __global__ void __launch_bounds__(128)
 #ifndef FS_MINB
 #define FS_MINB 6
 #endif
-constexpr int FS_TX = 16, FS_TY = 8, FS_NB = 16, FS_CAP = 8192;
+#ifndef CS_FS_CAP
+#define CS_FS_CAP 8192
+#endif
+constexpr int FS_TX = 16, FS_TY = 8, FS_NB = 16, FS_CAP = CS_FS_CAP;
 
 struct FsBox {
   int u0, v0, nu, nv, off;
@@ -254,12 +260,14 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
           const int u0 = (int)floor(uf);
           const float fu = (float)(uf - floor(uf));
           const float* pj = proj + (size_t)a0 * sheet;
+#pragma unroll
           for (int k = 0; k < FDK_ZB; k++) {
             const double vf =
                 ((wz0 + k * vz) * mag - off_v) * inv_dv + cv;
             const int v0 = (int)floor(vf);
             const float fv = (float)(vf - floor(vf));
             float t[4];
+#pragma unroll
             for (int q = 0; q < 4; q++) {
               const int u = u0 + (q & 1), v = v0 + (q >> 1);
               t[q] = (u >= 0 && u < n_u && v >= 0 && v < n_v)
