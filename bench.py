@@ -512,6 +512,14 @@ def run_extras(args, cs, K, g, vol, y, dev, rank, world, arange, zrange):
             torch.cuda.synchronize()
             ts[iters] = time.perf_counter() - t0
         out["sart_tv_s_per_iter"] = ts[2] - ts[1]
+        for iters in (1, 1, 3):
+            cfg = cs.ReconConfig(pool, cs.Algorithm.CGLS, iters)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            cs.cgls(b, g, cfg)
+            torch.cuda.synchronize()
+            ts[iters] = time.perf_counter() - t0
+        out["cgls_s_per_iter"] = (ts[3] - ts[1]) / 2
         cs.fdk(b, g, pool)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
