@@ -168,3 +168,39 @@ def test_fullsize_crop_vs_oracle(n, crop):
     print(f"n={n}: Ax relL2 {e_ax:.3e}, matched relL2 {e_b:.3e}, "
           f"FDK relL2 {e_f:.3e}")
     assert e_ax <= 1e-5 and e_b <= 1e-5 and e_f <= 1e-5, (e_ax, e_b, e_f)
+
+
+def test_config2_loops_properties():
+    """The loops at config-2 size (60 of the 360-view scan for speed):
+    CGLS residuals are monotone and drop; OS-SART and SART-TV
+    reduce ||b - A x||; SART-TV lowers the TV norm of the OS-SART result."""
+    import paper_1905_03748_b200 as cs
+    n = 512
+    full = synth_geometry(n, 360)
+    g = full.with_angles(full.angles[::6])
+    dev = torch.device("cuda", 0)
+    x_true = cs.phantom(cs.PhantomKind.SHEPP_LOGAN_3D, g.voxel_grid,
+                        device=dev).data
+    b = cs.forward_project_slab(cs.Volume(g.voxel_grid, x_true), g,
+                                (0, g.n_angles),
+                                cs.ProjectionMethod.INTERPOLATED)
+    pool = cs.DevicePool.b200(1)
+    r = cs.cgls(b, g, cs.ReconConfig(pool, cs.Algorithm.CGLS, 3))
+    res = r.residuals
+    assert all(b2 <= b1 * (1 + 1e-6) for b1, b2 in zip(res, res[1:])), res
+    assert res[-1] < 0.5 * res[0]
+
+    def resid(v):
+        ax = cs.forward_project_slab(cs.Volume(g.voxel_grid, v), g,
+                                     (0, g.n_angles),
+                                     cs.ProjectionMethod.INTERPOLATED).data
+        return float((ax - b.data).double().norm() / b.data.double().norm())
+
+    xo = cs.os_sart(b, g, cs.ReconConfig(pool, cs.Algorithm.OSSART, 2, 12)).data
+    assert resid(xo) < 0.5
+    tv = cs.TvParams(cs.TvMinimizer.GRADIENT_DESCENT, 1, 10, 5e-2)
+    xt = cs.os_sart(b, g, cs.ReconConfig(pool, cs.Algorithm.OSSART, 2, 12,
+                                         tv=tv)).data
+    assert resid(xt) < 0.6
+    tvn = lambda v: cs.tv_norm(cs.Volume(g.voxel_grid, v))
+    assert tvn(xt) < tvn(xo)
