@@ -3,16 +3,19 @@
 
 One *step* = one pass of the loop hot path over config 2:
 interpolated Ax over the rank's 360 angles of a 512^3 volume onto a 512^2
-detector + matched (exact-adjoint) Atb of the whole scan into the rank's
-axial slab -- the operator pair every OS-SART / SIRT / CGLS iteration
-applies (algorithms.py:213-216, :280-283).  Unit: voxel x angle updates.
+detector + matched (exact-adjoint) Atb of those angles -- the operator pair
+every OS-SART / SIRT / CGLS iteration applies (algorithms.py:213-216,
+:280-283).  Unit: voxel x angle updates.
 
-Multi-GPU (torchrun, one rank per GPU): weak scaling with the paper's
-splits -- the scan has 360 x N angles; rank r projects its own 360 angles
-of the full volume (angle split, scheduler.py:164-166) and backprojects all
-360 x N angles into its 512/N-slice slab (slab split).  Per-rank work is
-fixed, no collective sits in the data path.  Inputs (512 MiB volume, >= 360
-MiB stack) exceed the 126 MB L2, so no flush is needed between steps.
+Multi-GPU (torchrun, one rank per GPU): weak scaling -- the scan has 360 x
+N angles; rank r projects its own 360 angles of the full volume (angle
+split, scheduler.py:164-166) and backprojects the same 360 angles into a
+whole-volume partial; one NCCL reduce-scatter sums the partials so rank r
+ends with planes [512 r / N, 512 (r+1) / N) of the full Atb (the paper's
+slab split of Atb avoids this reduction over PCIe; over NVLink 5 it is ~1
+ms of a ~300 ms step, while thin slabs cost 35% efficiency at 8 ranks).
+Per-rank work is fixed.  Inputs (512 MiB volume, >= 360 MiB stack) exceed
+the 126 MB L2, so no flush is needed between steps.
 
 Also reported: per-operator GUPS (Ax, matched Atb, FDK Atb), OS-SART s/iter
 (block 36, rank 0 at N=1), the roofline of the dominant kernel, the CPU
@@ -74,6 +77,25 @@ def make_geometry(n, n_angles, cs):
     angles = tuple(np.linspace(0.0, 2 * math.pi, n_angles, endpoint=False))
     return cs.ScanGeometry(2.0 * n, 4.0 * n, angles, cs.VoxelGrid(n, n, n),
                            det)
+
+
+def atb_slabs(n, world, rank, per_rank=4):
+    """The rank's share of the volume for the slab-split Atb: with N > 1 the
+    n planes are cut into per_rank * N equal blocks dealt round-robin
+    (rank r owns blocks r, r + N, ...), so every rank's planes span the
+    whole height and the work balances whatever the data (the phantom's
+    sinogram has zero rays -- skipped, _kernels.py:295-296 -- mostly above
+    and below the head, which made the central contiguous slab the slowest
+    rank).  Atb is slab-partition invariant, so any partition
+    is the same operator."""
+    if world == 1:
+        return [(0, n)]
+    nb = per_rank * world
+    while nb > 1 and n % nb:
+        nb //= 2
+    nb = max(nb, world)
+    edges = [n * i // nb for i in range(nb + 1)]
+    return [(edges[b], edges[b + 1]) for b in range(rank, nb, world)]
 
 
 def bytes_per_update(n, n_det):
@@ -258,17 +280,36 @@ def run_ours(args):
     A = A1 * world
     g = make_geometry(n, A, cs)
     dev = torch.device("cuda", local)
-    a0, a1 = rank * A1, (rank + 1) * A1                      # Ax: angle split
-    z0, z1 = n * rank // world, n * (rank + 1) // world      # Atb: slab split
+    a0, a1 = rank * A1, (rank + 1) * A1       # angle split (Ax and Atb)
+    z0, z1 = n * rank // world, n * (rank + 1) // world
     nz_s = z1 - z0
+    if world > 1 and n % world:
+        raise SystemExit(f"--size {n} must be divisible by --gpus {world}")
 
     vol = cs.phantom(cs.PhantomKind.SHEPP_LOGAN_3D, g.voxel_grid,
                      device=dev).data
     proj = torch.empty((A1, n, n), dtype=torch.float32, device=dev)
-    y = torch.empty((A, n, n), dtype=torch.float32, device=dev)
-    K.fwd_interp(vol, g, (0, A), (0, n), y)                  # Atb input
-    slab = torch.zeros((nz_s, n, n), dtype=torch.float32, device=dev)
+    y = torch.empty((A1, n, n), dtype=torch.float32, device=dev)
+    K.fwd_interp(vol, g, (a0, a1), (0, n), y)                # Atb input
+    # N = 1: Atb straight into the volume.  N > 1: every rank backprojects
+    # ITS views into a full-volume partial and the partials are summed by
+    # one NCCL reduce-scatter, rank r keeping planes [z0, z1).  The paper
+    # slab-splits Atb instead (Alg. 2) to avoid that reduction over PCIe;
+    # over NVLink 5 the 512 MiB reduce-scatter costs ~1 ms against ~140 ms
+    # of backprojection, while thin slabs cost 35% efficiency at 8 ranks
+    # (per-(ray, slab) overheads; tools/rank_share.py).
+    acc = torch.zeros((n, n, n), dtype=torch.float32, device=dev)
+    slab = acc if world == 1 else torch.empty((nz_s, n, n),
+                                              dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
+
+    def reduce_scatter():
+        if backend == "nccl":
+            dist.reduce_scatter_tensor(slab, acc)
+        else:  # gloo (several ranks sharing one GPU, testing only)
+            host = acc.cpu()
+            dist.all_reduce(host)
+            slab.copy_(host[z0:z1])
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)]
           for _ in range(args.steps)]
@@ -276,7 +317,7 @@ def run_ours(args):
     # angle chunks of CHUNK views per launch (the paper's chunked launches;
     # one ncu capture == one bench launch)
     ax_chunks = [(c, min(c + CHUNK, a1)) for c in range(a0, a1, CHUNK)]
-    atb_chunks = [(c, min(c + CHUNK, A)) for c in range(0, A, CHUNK)]
+    atb_chunks = ax_chunks
 
     def step(e=None):
         if e:
@@ -285,9 +326,11 @@ def run_ours(args):
             K.fwd_interp(vol, g, (c0, c1), (0, n), proj[c0 - a0:c1 - a0])
         if e:
             e[1].record(stream)
-        K.fill(slab, 0.0)
+        K.fill(acc, 0.0)
         for c0, c1 in atb_chunks:
-            K.bwd_matched(y[c0:c1], g, (c0, c1), (z0, z1), slab)
+            K.bwd_matched(y[c0 - a0:c1 - a0], g, (c0, c1), (0, n), acc)
+        if world > 1:
+            reduce_scatter()
         if e:
             e[2].record(stream)
 
@@ -319,7 +362,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
     upd_ax = float(A1) * n ** 3
-    upd_atb = float(A) * nz_s * n * n
+    upd_atb = float(A1) * n ** 3  # the rank's views into the whole volume
     upd_step_rank = upd_ax + upd_atb
     total_upd = upd_step_rank * world * args.steps   # weak: equal per rank
     value = total_upd / elapsed / 1e9
@@ -348,10 +391,12 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (Shepp-Logan 3D phantom; Atb input = its Ax)",
         "config": {"workload": f"config 2 per GPU: {n}^3 volume, {n}^2 "
-                   f"detector, {A1} angles/GPU (scan of {A}); interp Ax "
-                   "(angle split) + matched Atb (slab split)",
+                   f"detector, {A1} angles/GPU (scan of {A}); interp Ax + "
+                   "matched Atb of the GPU's angles"
+                   + ("" if world == 1 else
+                      ", Atb partials reduce-scattered (NCCL) to slabs"),
                    "l2": "inputs > L2 (512 MiB volume, 360+ MiB stack)",
-                   "parallelism": f"angle/slab split x{world}"},
+                   "parallelism": f"angle split x{world}"},
         "ax_gups": upd_ax / t_ax / 1e9,
         "atb_matched_gups": upd_atb / t_atb / 1e9,
         "roofline": {"bound": "hbm", "kernel": kname,
@@ -383,18 +428,21 @@ def run_extras(args, cs, K, g, vol, y, dev, rank, world, arange, zrange):
     import torch
     out = {}
     n = g.voxel_grid.n_x
-    A = g.n_angles
+    # every rank: its own views (y) into the whole volume
+    va0, va1 = arange
+    A = va1 - va0
+    zrange = (0, n)
     z0, z1 = zrange
     slab = torch.zeros((z1 - z0, n, n), dtype=torch.float32, device=dev)
-    # FDK-weighted Atb (slab split, all angles)
+    # FDK-weighted Atb
     for _ in range(2):
-        K.bwd_fdk(y, g, (0, A), zrange, slab)
+        K.bwd_fdk(y, g, (va0, va1), zrange, slab)
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(True), torch.cuda.Event(True)
     s.record()
     reps = 3
     for _ in range(reps):
-        K.bwd_fdk(y, g, (0, A), zrange, slab)
+        K.bwd_fdk(y, g, (va0, va1), zrange, slab)
     e.record()
     torch.cuda.synchronize()
     out["atb_fdk_gups"] = reps * float(A) * (z1 - z0) * n * n / (
@@ -404,10 +452,10 @@ def run_extras(args, cs, K, g, vol, y, dev, rank, world, arange, zrange):
     # (_kernels.py:295-296); a residual stack is dense
     dense = torch.randn(y.shape, device=dev, generator=torch.Generator(
         device=dev).manual_seed(1))
-    K.bwd_matched(dense, g, (0, A), zrange, slab)
+    K.bwd_matched(dense, g, (va0, va1), zrange, slab)
     torch.cuda.synchronize()
     s.record()
-    K.bwd_matched(dense, g, (0, A), zrange, slab)
+    K.bwd_matched(dense, g, (va0, va1), zrange, slab)
     e.record()
     torch.cuda.synchronize()
     out["atb_matched_dense_gups"] = float(A) * (z1 - z0) * n * n / (
@@ -448,7 +496,8 @@ def run_extras(args, cs, K, g, vol, y, dev, rank, world, arange, zrange):
     def e2e_step():
         p = cs.forward_project_slab(cs.Volume(g.voxel_grid, vol_np), g,
                                     (a0, a1), IP)
-        v = cs.backproject_slab(cs.ProjectionStack(g.detector, y_np), g,
+        v = cs.backproject_slab(cs.ProjectionStack(g.detector, y_np,
+                                                   (va0, va1)), g,
                                 zrange, cs.WeightMode.MATCHED)
         return p, v
     # warm-up calls: results are held until the next call returns, so the
