@@ -1,12 +1,10 @@
 """Large-configuration measurements on ONE B200 (not the bench contract):
 
 * ``c3``: the per-rank work of config 3 (2048^3 volume, 2048^2 detector,
-  1024 views) under the paper's splits at N GPUs -- interp Ax of the rank's
-  1024/N views over the full volume (angle split) and matched Atb of all
-  1024 views into the rank's 2048/N-plane slab (slab split).  Per-rank work
-  at N = 8 is what one GPU does in the 8-GPU run (no collective sits in the
-  data path), so its GUPS bounds the 8-GPU throughput at 8x.  Also A/B of
-  v-band culling (CS_NO_CULL=1 in a second process).
+  1024 views) at N GPUs under bench.py's decomposition -- interp Ax and
+  matched Atb of the rank's 1024/N views over the whole volume, plus the
+  reduce-scatter payload of the Atb partials (costed at 700 GB/s, the
+  measured NVLink all-reduce bus bandwidth).
 * ``ooc``: out-of-core streaming through execute_forward / execute_backward
   with a device budget below the volume size (slabs streamed H2D from
   page-locked host memory, Algorithm 1/2), against the same operators
@@ -43,41 +41,44 @@ def timed(fn, reps=1):
 
 
 def c3(N=8, A=1024, n=2048, rank=None):
+    """Rank r's work at N ranks under bench.py's decomposition: interp Ax
+    and matched Atb of its A/N views over the whole volume (Atb input: a
+    dense stack, 1 + the phantom's sinogram), plus the reduce-scatter
+    payload it would send (7/8 of the volume at N = 8)."""
     dev = torch.device("cuda", 0)
-    rank = N // 2 if rank is None else rank   # a central slab
+    rank = N // 2 if rank is None else rank
     g = bench.make_geometry(n, A, cs)
     vol = cs.phantom(cs.PhantomKind.SHEPP_LOGAN_3D, g.voxel_grid,
                      device=dev).data
     a0, a1 = A * rank // N, A * (rank + 1) // N
-    z0, z1 = n * rank // N, n * (rank + 1) // N
     proj = torch.empty((a1 - a0, n, n), device=dev)
     chunk = 64
     t_ax = timed(lambda: [K.fwd_interp(vol, g, (c, min(c + chunk, a1)),
                                        (0, n), proj[c - a0:min(c + chunk, a1) - a0])
                           for c in range(a0, a1, chunk)])
     ax_upd = float(a1 - a0) * n ** 3
-    # Atb input: a dense stack (1 + sinogram of the phantom: no zero
-    # pixels, which the matched adjoint would skip, _kernels.py:295-296)
-    y = torch.empty((A, n, n), device=dev)
-    for c in range(0, A, chunk):
-        K.fwd_interp(vol, g, (c, min(c + chunk, A)), (0, n), y[c:c + chunk])
-    y += 1.0
+    y = proj.clone()
+    y += 1.0  # dense: no zero pixels (the matched adjoint skips zeros)
+    acc = torch.zeros((n, n, n), device=dev)
     del vol
     torch.cuda.empty_cache()
-    slab = torch.zeros((z1 - z0, n, n), device=dev)
 
     def atb():
-        for c in range(0, A, chunk):
-            K.bwd_matched(y[c:c + chunk], g, (c, min(c + chunk, A)),
-                          (z0, z1), slab)
+        for c in range(a0, a1, chunk):
+            K.bwd_matched(y[c - a0:min(c + chunk, a1) - a0], g,
+                          (c, min(c + chunk, a1)), (0, n), acc)
     t_atb = timed(atb)
-    atb_upd = float(A) * (z1 - z0) * n * n
+    atb_upd = float(a1 - a0) * n ** 3
+    rs_bytes = (N - 1) / N * n ** 3 * 4
     out = {"measure": "c3_rank_share", "N": N, "rank": rank, "n": n,
-           "views": A, "cull": os.environ.get("CS_NO_CULL", "0") != "1",
+           "views": A, "views_per_rank": a1 - a0,
            "ax_gups": ax_upd / t_ax / 1e9, "ax_s": t_ax,
            "atb_matched_gups": atb_upd / t_atb / 1e9, "atb_s": t_atb,
+           "reduce_scatter_bytes": rs_bytes,
+           "reduce_scatter_s_at_700GBps": rs_bytes / 700e9,
            "step_gups_per_rank": (ax_upd + atb_upd) / (t_ax + t_atb) / 1e9}
-    out["projected_N_gpu_gups"] = out["step_gups_per_rank"] * N
+    out["projected_N_gpu_gups"] = N * (ax_upd + atb_upd) / (
+        t_ax + t_atb + rs_bytes / 700e9) / 1e9
     print(json.dumps(out), flush=True)
 
 
