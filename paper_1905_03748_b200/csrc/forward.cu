@@ -105,7 +105,10 @@ __global__ void __launch_bounds__(128, FWD_MINB)
 }
 
 // Siddon traversal, _kernels.py:71-151 (fp64, midpoint attribution).
-__global__ void __launch_bounds__(128)
+#ifndef SID_MINB
+#define SID_MINB 10  // <= 48 registers: 40 warps/SM hide the fp64 chain latency
+#endif
+__global__ void __launch_bounds__(128, SID_MINB)
     fwd_siddon_kernel(const float* __restrict__ vol,
                       const AngleGeom* __restrict__ geom, Grid G, int z_lo,
                       int z_hi, int n_u, int n_v, int v_base, int v_end,
