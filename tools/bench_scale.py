@@ -10,7 +10,16 @@
   page-locked host memory, Algorithm 1/2), against the same operators
   in-core.
 
+* ``c5``: config 5 scale on ONE GPU without ever materialising the volume:
+  a 4096^3 Shepp-Logan (256 GiB, > one B200's HBM) is generated slab by
+  slab on the device, projected slab by slab with the partial projections
+  accumulated in the kernel epilogue (Algorithm 1), then backprojected
+  slab by slab (Algorithm 2) while the adjoint identity <A x, y> =
+  <x, A^T y> is accumulated across slabs in fp64 -- a full-scale
+  consistency check of both operators at 4096^3.
+
     python tools/bench_scale.py c3 [N=8] [views=1024]
+    python tools/bench_scale.py c5 [n=4096] [views=32] [slab=256]
     python tools/bench_scale.py ooc [n=2048] [views=64] [budget_gib=12]
 
 Prints one JSON line per measurement.
@@ -151,10 +160,85 @@ def ooc(n=2048, A=64, budget_gib=12.0):
                       "volume_gib": n ** 3 * 4 / 2 ** 30, **res}), flush=True)
 
 
+def _phantom_slab(g, z0, z1, dev):
+    """Shepp-Logan values of planes [z0, z1) of g's grid (fp32 on the
+    device; the same formula as paper_1905_03748_b200.phantoms)."""
+    from paper_1905_03748_b200.phantoms import SHEPP_LOGAN_ELLIPSOIDS
+    import math
+    grid = g.voxel_grid
+    ex, ey, ez = grid.extent
+    vx, vy, vz = grid.voxel_size
+
+    def centres(a, b, v, e):
+        return ((torch.arange(a, b, dtype=torch.float64, device=dev) + 0.5)
+                * v - 0.5 * e) / (0.5 * e)
+    x = centres(0, grid.n_x, vx, ex).float()[None, None, :]
+    y = centres(0, grid.n_y, vy, ey).float()[None, :, None]
+    z = centres(z0, z1, vz, ez).float()[:, None, None]
+    out = torch.zeros((z1 - z0, grid.n_y, grid.n_x), device=dev)
+    for value, a, b, c, x0, y0, zc, phi_deg in SHEPP_LOGAN_ELLIPSOIDS:
+        zz = ((z - zc) / c) ** 2
+        if float(zz.min()) > 1.0:
+            continue
+        phi = math.radians(phi_deg)
+        cp, sp = math.cos(phi), math.sin(phi)
+        xr = (x - x0) * cp + (y - y0) * sp
+        yr = -(x - x0) * sp + (y - y0) * cp
+        out += value * (((xr / a) ** 2 + (yr / b) ** 2 + zz) <= 1.0)
+    return out
+
+
+def c5(n=4096, A=32, slab=256):
+    dev = torch.device("cuda", 0)
+    g = bench.make_geometry(n, A, cs)
+    slabs = [(z, min(z + slab, n)) for z in range(0, n, slab)]
+    proj = torch.empty((A, n, n), device=dev)
+    torch.cuda.synchronize()
+    t_gen = t_fwd = t_bwd = 0.0
+    for si, (z0, z1) in enumerate(slabs):
+        t0 = time.perf_counter()
+        xs = _phantom_slab(g, z0, z1, dev)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        K.fwd_interp(xs, g, (0, A), (z0, z1), proj, accumulate=si > 0)
+        torch.cuda.synchronize()
+        t_fwd += time.perf_counter() - t1
+        t_gen += t1 - t0
+        del xs
+    # y = a dense stack (no zero pixels); <A x, y> in fp64
+    y = proj + 1.0
+    lhs = sum(float((proj[a].double() * y[a].double()).sum())
+              for a in range(A))
+    rhs = 0.0
+    acc = torch.empty((slab, n, n), device=dev)
+    for z0, z1 in slabs:
+        xs = _phantom_slab(g, z0, z1, dev)
+        a_ = acc[:z1 - z0]
+        a_.zero_()
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        K.bwd_matched(y, g, (0, A), (z0, z1), a_)
+        torch.cuda.synchronize()
+        t_bwd += time.perf_counter() - t1
+        rhs += sum(float((xs[k].double() * a_[k].double()).sum())
+                   for k in range(z1 - z0))
+        del xs
+    upd = float(A) * n ** 3
+    print(json.dumps({
+        "measure": "c5_slab_streamed", "n": n, "views": A,
+        "volume_gib": n ** 3 * 4 / 2 ** 30, "slab_planes": slab,
+        "slabs": len(slabs), "ax_s": t_fwd, "ax_gups": upd / t_fwd / 1e9,
+        "atb_matched_s": t_bwd, "atb_matched_gups": upd / t_bwd / 1e9,
+        "phantom_gen_s": t_gen, "adjoint_lhs": lhs, "adjoint_rhs": rhs,
+        "adjoint_rel_diff": abs(lhs - rhs) / abs(lhs)}), flush=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1]
     args = [float(a) for a in sys.argv[2:]]
     if what == "c3":
         c3(*[int(a) for a in args])
+    elif what == "c5":
+        c5(*[int(a) for a in args])
     else:
         ooc(*([int(args[0])] if args else []) + ([int(args[1])] if len(args) > 1 else []) + (args[2:3]))
