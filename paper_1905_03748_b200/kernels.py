@@ -17,6 +17,21 @@ from .geometry import ScanGeometry, VoxelGrid, flat_geometry, grid6
 MAX_ANGLES_PER_LAUNCH = 65535  # grid.z limit of the ray kernels
 
 
+def _checked_retry_oom(call):
+    """check(call()); if the library ran out of device memory (its texture
+    arrays and stream-ordered tables are allocated outside torch), release
+    torch's cached blocks and retry once.  The C-ABI allocates before it
+    launches anything, so a failed call left no partial result."""
+    rc = call()
+    if rc != 0:
+        msg = lib().cs_last_error().decode()
+        if "out of memory" in msg:
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+            rc = call()
+    check(rc)
+
+
 def launch_count() -> int:
     """Kernels the library has launched since it was loaded."""
     return int(lib().cs_launch_count())
@@ -51,7 +66,7 @@ def fwd_interp(vol: torch.Tensor, geometry: ScanGeometry, angle_range,
     L = lib()
     for c0, c1 in _angle_chunks(a0, a1):
         geom = flat_geometry(geometry, c0, c1)
-        check(L.cs_fwd_interp(
+        _checked_retry_oom(lambda: L.cs_fwd_interp(
             dptr(vol), grid.n_x, grid.n_y, grid.n_z, z_lo, z_hi, hptr(g6),
             hptr(geom), c1 - c0, det.n_u, det.n_v, step,
             dptr(out[c0 - a0:c1 - a0]), int(accumulate), stream_ptr(stream)))
@@ -74,7 +89,7 @@ def fwd_interp_residual(vol: torch.Tensor, geometry: ScanGeometry,
     for c0, c1 in _angle_chunks(a0, a1):
         geom = flat_geometry(geometry, c0, c1)
         sl = slice(c0 - a0, c1 - a0)
-        check(L.cs_fwd_interp_residual(
+        _checked_retry_oom(lambda: L.cs_fwd_interp_residual(
             dptr(vol), grid.n_x, grid.n_y, grid.n_z, hptr(g6), hptr(geom),
             c1 - c0, det.n_u, det.n_v, step, dptr(b[sl]),
             None if w is None else dptr(w[sl]), dptr(out[sl]),
