@@ -23,6 +23,7 @@
 // shared-memory budget are served from global memory for that chunk.
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -42,6 +43,8 @@ constexpr int ST_S = CS_ST_S;  // planes per chunk along the main axis
 // quarter of the FMA rate on sm_100 and the matched deposit needed 8 of
 // them per sample for its fixed-point taps; this is one FFMA + IADD.
 constexpr float ST_MAGIC = 12582912.f;
+// largest fixed-point tap: |x| < 2^22 keeps the magic add exact
+constexpr double ST_BUDGET_CAP = 4.0e6;
 __device__ __forceinline__ int magic_int(float biased) {
   return __float_as_int(biased) - 0x4B400000;
 }
@@ -58,7 +61,12 @@ __device__ __forceinline__ void st_red4(float* p, float a, float b, float c,
                : "memory");
 }
 
-template <int OP, int M, int MODE>
+// WIDE (matched only): int64 box accumulators.  The int32 box must keep
+// every per-voxel chunk sum below 2^31, so its fixed-point scale shrinks
+// when many rays cross a voxel (detector pixels much finer than voxels:
+// fixed_point_budget); there the 64-bit box keeps the full 2^-22-of-max-tap
+// resolution at twice the shared memory per entry.
+template <int OP, int M, int MODE, bool WIDE = false>
 __global__ void __launch_bounds__(ST_THREADS, 3)
     staged_kernel(const float* __restrict__ vol_in, float* __restrict__ vol_acc,
                   const AngleGeom* __restrict__ geom,
@@ -68,8 +76,18 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
                   const float* __restrict__ rb, const float* __restrict__ rw,
                   int box_cap, float fx_budget, int vec_ok) {
   constexpr int T = 1 - M;
-  extern __shared__ float st_box[];
-  int* box_i = reinterpret_cast<int*>(st_box);
+  using Acc = typename std::conditional<WIDE, long long, int>::type;
+  extern __shared__ float4 st_box4[];
+  float* st_box = reinterpret_cast<float*>(st_box4);
+  Acc* box_i = reinterpret_cast<Acc*>(st_box4);
+  box_cap = WIDE ? box_cap / 2 : box_cap;  // in accumulator entries
+  auto deposit = [](Acc* a, int v) {
+    if (WIDE)
+      atomicAdd(reinterpret_cast<unsigned long long*>(a),
+                (unsigned long long)(long long)v);
+    else
+      atomicAdd(reinterpret_cast<int*>(a), v);
+  };
   __shared__ int ext[8];   // mlo, mhi, -, -, -, -, dir flags
   __shared__ int ext8[8];  // per chunk candidate: tlo, thi, zlo, zhi (x2)
   __shared__ float s_scale;
@@ -359,14 +377,14 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
             const float z0 = sv * (1.f - wz), z1 = sv * wz;
             const float y00 = z0 * (1.f - wy), y01 = z0 * wy;
             const float y10 = z1 * (1.f - wy), y11 = z1 * wy;
-            atomicAdd(&box_i[b], magic_int(fmaf(y00, 1.f - wx, ST_MAGIC)));
-            atomicAdd(&box_i[b + sx], magic_int(fmaf(y00, wx, ST_MAGIC)));
-            atomicAdd(&box_i[b + sy], magic_int(fmaf(y01, 1.f - wx, ST_MAGIC)));
-            atomicAdd(&box_i[b + sy + sx], magic_int(fmaf(y01, wx, ST_MAGIC)));
-            atomicAdd(&box_i[b + sz], magic_int(fmaf(y10, 1.f - wx, ST_MAGIC)));
-            atomicAdd(&box_i[b + sz + sx], magic_int(fmaf(y10, wx, ST_MAGIC)));
-            atomicAdd(&box_i[b + sz + sy], magic_int(fmaf(y11, 1.f - wx, ST_MAGIC)));
-            atomicAdd(&box_i[b + sz + sy + sx], magic_int(fmaf(y11, wx, ST_MAGIC)));
+            deposit(&box_i[b], magic_int(fmaf(y00, 1.f - wx, ST_MAGIC)));
+            deposit(&box_i[b + sx], magic_int(fmaf(y00, wx, ST_MAGIC)));
+            deposit(&box_i[b + sy], magic_int(fmaf(y01, 1.f - wx, ST_MAGIC)));
+            deposit(&box_i[b + sy + sx], magic_int(fmaf(y01, wx, ST_MAGIC)));
+            deposit(&box_i[b + sz], magic_int(fmaf(y10, 1.f - wx, ST_MAGIC)));
+            deposit(&box_i[b + sz + sx], magic_int(fmaf(y10, wx, ST_MAGIC)));
+            deposit(&box_i[b + sz + sy], magic_int(fmaf(y11, 1.f - wx, ST_MAGIC)));
+            deposit(&box_i[b + sz + sy + sx], magic_int(fmaf(y11, wx, ST_MAGIC)));
           }
         } else {
           // overflow path: straight from / to global memory
@@ -405,19 +423,22 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
       for (int qi = threadIdx.x; qi < nquads;
            qi += ST_THREADS, quad_next(xq, by, bz)) {
         const int d = bz * sz + by * sy + 4 * xq * sx;
-        int4 q;
-        if (M == 1) {
-          q = *reinterpret_cast<const int4*>(box_i + d);
+        Acc q0, q1, q2, q3;
+        if (M == 1 && !WIDE) {
+          const int4 q = *reinterpret_cast<const int4*>(box_i + d);
+          q0 = q.x; q1 = q.y; q2 = q.z; q3 = q.w;
         } else {
-          q = make_int4(box_i[d], box_i[d + sx], box_i[d + 2 * sx],
-                        box_i[d + 3 * sx]);
+          q0 = box_i[d];
+          q1 = box_i[d + sx];
+          q2 = box_i[d + 2 * sx];
+          q3 = box_i[d + 3 * sx];
         }
-        if ((q.x | q.y | q.z | q.w) == 0) continue;
+        if ((q0 | q1 | q2 | q3) == 0) continue;
         const int gx = bo[0] + 4 * xq, gy = bo[1] + by, gz = bo[2] + bz;
         if (gy < 0 || gy >= ny || gz < z_lo || gz >= z_hi) continue;
         float* dst = vol_acc + (size_t)(gz - z_lo) * plane + (size_t)gy * nx;
-        const float f0 = (float)q.x * inv_scale, f1 = (float)q.y * inv_scale;
-        const float f2 = (float)q.z * inv_scale, f3 = (float)q.w * inv_scale;
+        const float f0 = (float)q0 * inv_scale, f1 = (float)q1 * inv_scale;
+        const float f2 = (float)q2 * inv_scale, f3 = (float)q3 * inv_scale;
         if (vec_ok && gx >= 0 && gx + 3 < nx) {
           st_red4(dst + gx, f0, f1, f2, f3);
         } else {
@@ -488,7 +509,7 @@ static float fixed_point_budget(const double* grid6, int nx, int ny, int nz,
   // every tap |val * step * w| * scale <= b must stay below 2^22 for the
   // magic-number conversion (ST_MAGIC): resolution 2.5e-7 of the CTA's
   // largest tap
-  if (b > 4.0e6) b = 4.0e6;
+  if (b > ST_BUDGET_CAP) b = ST_BUDGET_CAP;
   return (float)b;
 }
 
@@ -542,10 +563,14 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   static const char* kb_knob = getenv("CS_STAGED_SMEM_KB");
   const size_t smem = (kb_knob ? (size_t)atoi(kb_knob) : 64) * 1024;
   const int cap = (int)(smem / sizeof(float));
-  const float budget =
+  float budget =
       OP == OP_BWD ? fixed_point_budget(grid6, nx, ny, nz, geom, n_a, n_u, n_v,
                                         step_max)
                    : 0.f;
+  // int32 boxes while their budget reaches the magic-add cap (every
+  // production geometry so far); int64 boxes at the cap otherwise
+  const bool wide = OP == OP_BWD && budget < ST_BUDGET_CAP;
+  if (wide) budget = ST_BUDGET_CAP;
   const void* vbase = OP == OP_BWD ? (const void*)vol_acc : (const void*)vol_in;
   const int vec_ok = (nx % 4 == 0) && (((uintptr_t)vbase & 15) == 0);
   // v-band culling per main-axis class (runtime.cu slab_row_band); the
@@ -595,8 +620,8 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   auto rows = [&](int c) {
     return (unsigned)((band[c][1] - band[c][0] + ST_TV - 1) / ST_TV);
   };
-  auto k0 = staged_kernel<OP, 0, MODE>;
-  auto k1 = staged_kernel<OP, 1, MODE>;
+  auto k0 = wide ? staged_kernel<OP, 0, MODE, true> : staged_kernel<OP, 0, MODE>;
+  auto k1 = wide ? staged_kernel<OP, 1, MODE, true> : staged_kernel<OP, 1, MODE>;
   // the dynamic shared-memory opt-in is per device: set it once on each
   // (the executor drives several GPUs from one process)
   static std::atomic<unsigned long long> attr_done{0};
@@ -604,10 +629,11 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   cudaGetDevice(&dev_ord);
   const unsigned long long bit = 1ull << (dev_ord & 63);
   if (!(attr_done.load() & bit)) {
-    cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-    cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
+    for (auto k : {staged_kernel<OP, 0, MODE>, staged_kernel<OP, 1, MODE>,
+                   staged_kernel<OP, 0, MODE, true>,
+                   staged_kernel<OP, 1, MODE, true>})
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
     attr_done.fetch_or(bit);
   }
   if (nxm > 0 && rows(0) > 0) {
