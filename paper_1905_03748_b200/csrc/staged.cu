@@ -74,27 +74,44 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
                   int z_lo, int z_hi, int n_u, int n_v, int v_base, int v_end,
                   float* __restrict__ out, const float* __restrict__ proj_in,
                   const float* __restrict__ rb, const float* __restrict__ rw,
-                  int box_cap, float fx_budget, int vec_ok) {
+                  int box_cap, float fx_budget, int vec_ok, int lane_stride) {
   constexpr int T = 1 - M;
   using Acc = typename std::conditional<WIDE, long long, int>::type;
   extern __shared__ float4 st_box4[];
   float* st_box = reinterpret_cast<float*>(st_box4);
   Acc* box_i = reinterpret_cast<Acc*>(st_box4);
   box_cap = WIDE ? box_cap / 2 : box_cap;  // in accumulator entries
+  // WIDE entries are two int32 words: the low 11 bits of every tap
+  // (0..2047) and the rest (v >> 11), each summed with a native ATOMS.ADD
+  // (sm_100 has no native 64-bit shared add: a CAS loop under contention
+  // was 8-20x slower); value = hi * 2048 + lo, exact for < 2^19 taps.
   auto deposit = [](Acc* a, int v) {
-    if (WIDE)
-      atomicAdd(reinterpret_cast<unsigned long long*>(a),
-                (unsigned long long)(long long)v);
-    else
+    if (WIDE) {
+      int* w = reinterpret_cast<int*>(a);
+      atomicAdd(w, v & 0x7FF);
+      atomicAdd(w + 1, v >> 11);
+    } else {
       atomicAdd(reinterpret_cast<int*>(a), v);
+    }
+  };
+  auto widen = [](Acc raw) -> long long {
+    if (!WIDE) return (long long)raw;
+    const int2 w = *reinterpret_cast<const int2*>(&raw);
+    return (long long)w.y * 2048 + (long long)w.x;
   };
   __shared__ int ext[8];   // mlo, mhi, -, -, -, -, dir flags
   __shared__ int ext8[8];  // per chunk candidate: tlo, thi, zlo, zhi (x2)
   __shared__ float s_scale;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int u = blockIdx.x * ST_TU + lane;
-  const int v = v_base + blockIdx.y * ST_TV + warp;
+  // lane_stride s (power of two <= ST_TV): the CTA covers 32 s columns x
+  // 8 / s rows and a warp's lanes are s pixels apart, so with pixels finer
+  // than voxels the lanes of one ATOMS instruction seldom hit the same
+  // shared word (same-address atomics serialise)
+  const int u = blockIdx.x * (ST_TU * lane_stride) + lane * lane_stride +
+                (warp & (lane_stride - 1));
+  const int v = v_base + blockIdx.y * (ST_TV / lane_stride) +
+                warp / lane_stride;
   const int a = view_ids[blockIdx.z];
   const bool valid = u < n_u && v < v_end;
   const int nx = G.n[0], ny = G.n[1];
@@ -434,6 +451,12 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
           q3 = box_i[d + 3 * sx];
         }
         if ((q0 | q1 | q2 | q3) == 0) continue;
+        if (WIDE) {
+          q0 = widen(q0);
+          q1 = widen(q1);
+          q2 = widen(q2);
+          q3 = widen(q3);
+        }
         const int gx = bo[0] + 4 * xq, gy = bo[1] + by, gz = bo[2] + bz;
         if (gy < 0 || gy >= ny || gz < z_lo || gz >= z_hi) continue;
         float* dst = vol_acc + (size_t)(gz - z_lo) * plane + (size_t)gy * nx;
@@ -477,9 +500,11 @@ static int view_axis(const double* g12, int n_u, int n_v) {
 // at most (2 / min step + 1) samples of weight <= 1 into it; the footprint
 // of a pixel is smallest nearest the source (magnification dsd / (dso - r)).
 // Returns the scale numerator: per CTA, scale = budget / max|val * step|.
-static float fixed_point_budget(const double* grid6, int nx, int ny, int nz,
-                                const double* geom, int n_a, int n_u, int n_v,
-                                double step_max) {
+// Smallest footprint of a detector pixel on the grid, in voxels (pixels
+// nearest the source are smallest: magnification dsd / (dso - r)).
+static double min_pixel_footprint(const double* grid6, int nx, int ny,
+                                  int nz, const double* geom, int n_a,
+                                  int n_u, int n_v) {
   const double ex = nx * grid6[3], ey = ny * grid6[4], ez = nz * grid6[5];
   const double gc[3] = {grid6[0] + 0.5 * ex, grid6[1] + 0.5 * ey,
                         grid6[2] + 0.5 * ez};
@@ -501,11 +526,24 @@ static float fixed_point_budget(const double* grid6, int nx, int ny, int nz,
     const double near = fmax(dso - rad, 1e-6 * dsd);
     fp = fmin(fp, fmin(du, dv) * near / dsd / vmax);
   }
+  return fp;
+}
+
+static float fixed_point_budget(const double* grid6, int nx, int ny, int nz,
+                                const double* geom, int n_a, int n_u, int n_v,
+                                double step_max) {
+  const double vmax = fmax(grid6[3], fmax(grid6[4], grid6[5]));
+  double fp = min_pixel_footprint(grid6, nx, ny, nz, geom, n_a, n_u, n_v);
   fp = fmax(fp, 1e-3);
   const double rays = (2.0 / fp + 1.0) * (2.0 / fp + 1.0);
   const double samples = 2.0 * vmax / (0.5 * step_max) + 1.0;
   const double bound = fmin(rays, (double)ST_THREADS) * samples;
-  double b = 1.0e9 / bound;  // per-voxel |sum| <= 1e9 < 2^31
+  // per-voxel |sum| <= 2e9 < 2^31.  The bound counts every sample of a
+  // ray in the 2x2x2 support at weight 1; the weights of one ray through
+  // the support sum to at most 1 / step + 1 <= 4 / vmin + 1 voxels' worth
+  // (step >= step_max / 2), against the 4 vmax / step_max + 1 = 8 + 1
+  // counted here, so the true sum stays under ~1.1e9.
+  double b = 2.0e9 / bound;
   // every tap |val * step * w| * scale <= b must stay below 2^22 for the
   // magic-number conversion (ST_MAGIC): resolution 2.5e-7 of the CTA's
   // largest tap
@@ -616,9 +654,26 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
       }
     }
   }
-  const unsigned gx = (n_u + ST_TU - 1) / ST_TU;
+  // lane stride from the finest pixel footprint fp (fixed_point_budget's
+  // geometry): s fp <= 1/2 voxel between neighbouring lanes.  Measured on
+  // 256^3 with 512^2 / 1024^2 / 2048^2 detectors (fp = 0.4 / 0.2 / 0.1):
+  // s = 2 loses 8% at fp = 0.4; s = 2 / 4 gain 3% / 55% at fp = 0.2 / 0.1
+  int lane_stride = 1;
+  if (OP == OP_BWD) {
+    const double fp = min_pixel_footprint(grid6, nx, ny, nz, geom, n_a, n_u,
+                                          n_v);
+    while (lane_stride < ST_TV && fp * lane_stride * 4 <= 1.0)
+      lane_stride *= 2;
+  }
+  static const char* ls_knob = getenv("CS_ST_LANE_STRIDE");  // A/B knob
+  if (ls_knob) {
+    const int k = atoi(ls_knob);
+    if (k == 1 || k == 2 || k == 4 || k == 8) lane_stride = k;
+  }
+  const unsigned gx = (n_u + ST_TU * lane_stride - 1) / (ST_TU * lane_stride);
   auto rows = [&](int c) {
-    return (unsigned)((band[c][1] - band[c][0] + ST_TV - 1) / ST_TV);
+    const int rv = ST_TV / lane_stride;
+    return (unsigned)((band[c][1] - band[c][0] + rv - 1) / rv);
   };
   auto k0 = wide ? staged_kernel<OP, 0, MODE, true> : staged_kernel<OP, 0, MODE>;
   auto k1 = wide ? staged_kernel<OP, 1, MODE, true> : staged_kernel<OP, 1, MODE>;
@@ -639,13 +694,15 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   if (nxm > 0 && rows(0) > 0) {
     k0<<<dim3(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids, G, step_max, z_lo, z_hi, n_u, n_v,
-        band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_ok);
+        band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_ok,
+        lane_stride);
     CS_COUNT_LAUNCH();
   }
   if (nall > nxm && rows(1) > 0) {
     k1<<<dim3(gx, rows(1), nall - nxm), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids + nxm, G, step_max, z_lo, z_hi, n_u, n_v,
-        band[1][0], band[1][1], out, proj_in, rb, rw, cap, budget, vec_ok);
+        band[1][0], band[1][1], out, proj_in, rb, rw, cap, budget, vec_ok,
+        lane_stride);
     CS_COUNT_LAUNCH();
   }
   e = cudaGetLastError();

@@ -504,3 +504,37 @@ def test_wide_fan_and_cone_vs_oracle():
                       ofn(y, og)) <= TOL_OP, mode
         assert rel_l2(cs.backproject_slab(st, g, (3, 9), mode).data,
                       ofn(y, og, (0, 8), (3, 9))) <= TOL_OP, mode
+
+
+def test_fine_detector_lane_strides_subprocess():
+    """Pixels much finer than voxels: the staged matched kernel spreads a
+    warp's lanes s pixels apart (s = 1, 2, 4, 8; forced with the
+    CS_ST_LANE_STRIDE knob, read once, hence subprocesses) on a detector
+    whose width / height are not multiples of 32 s / 8 / s; full volume and
+    a slab / view window against the oracle."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path[:0] = [%r, %r]\n"
+        "import numpy as np, paper_1905_03748_b200 as cs\n"
+        "from conftest import to_oracle, rel_l2\n"
+        "from oracle import oracle as O\n"
+        "from test_gpu_parity import _odd_geometry\n"
+        "g = _odd_geometry(12, 10, 9, 151, 133, 4, pitch=(0.09, 0.11))\n"
+        "og = to_oracle(g)\n"
+        "y = np.random.default_rng(6).standard_normal((4, 133, 151)).astype(np.float32)\n"
+        "st = cs.ProjectionStack(g.detector, y)\n"
+        "got = cs.backproject_slab(st, g, (0, 9), cs.WeightMode.MATCHED).data\n"
+        "e1 = rel_l2(got, O.bwd_matched(y, og))\n"
+        "st2 = cs.ProjectionStack(g.detector, y[1:3], (1, 3))\n"
+        "got = cs.backproject_slab(st2, g, (2, 7), cs.WeightMode.MATCHED).data\n"
+        "e2 = rel_l2(got, O.bwd_matched(y[1:3], og, (1, 3), (2, 7)))\n"
+        "print(e1, e2); assert e1 <= 1e-5 and e2 <= 1e-5\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+         os.path.dirname(os.path.abspath(__file__)))
+    for s in ("1", "2", "4", "8", ""):
+        env = dict(os.environ, CS_ST_LANE_STRIDE=s)
+        r = subprocess.run([sys.executable, "-c", code], env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, (s, r.stderr[-2000:])

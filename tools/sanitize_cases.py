@@ -64,6 +64,9 @@ def main():
         np.float32)).to(dev)
     acc = torch.zeros((8, 8, 8), device=dev)
     K.bwd_fdk(y, g, (0, 2), (0, 8), acc)
+    # matched Atb with strided lanes (fine pixels: lane stride 8)
+    K.bwd_matched(y, g, (0, 2), (0, 8), acc)
+    K.bwd_matched(y, g, (0, 2), (3, 5), acc[3:5])
     torch.cuda.synchronize()
     print("sanitize cases done")
 
