@@ -249,6 +249,17 @@ __device__ __forceinline__ float4 gather_a2d(cudaTextureObject_t t, int layer,
   return r;
 }
 
+// gather_a2d into r only where p holds (predicated tld4: a quad whose lanes
+// are all off costs the texture pipe nothing; r keeps its value elsewhere)
+__device__ __forceinline__ void gather_a2d_if(float4& r, bool p,
+                                              cudaTextureObject_t t,
+                                              int layer, float x, float y) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %9, 0;\n\t"
+      "@q tld4.r.a2d.v4.f32.f32 {%0, %1, %2, %3}, [%4, {%5, %6, %7, %8}];\n\t}"
+      : "+f"(r.x), "+f"(r.y), "+f"(r.z), "+f"(r.w)
+      : "l"(t), "r"(layer), "f"(x), "f"(y), "f"(0.f), "r"((int)p));
+}
+
 // ---------------------------------------------------------------------------
 // Host side: per-(device, stream) layered-texture cache.  A volume slab
 // [n_slab, ny, nx] becomes a cudaArray with nx x ny layers; a projection
@@ -262,12 +273,26 @@ struct LayeredTexture {
 
 // TEX_VOLUME: a volume slab as z-layers (x, y per layer);
 // TEX_PROJ: a projection stack as angle-layers (u, v per layer).
-enum TexRole { TEX_VOLUME = 0, TEX_PROJ = 1 };
+// TEX_VOL_M / TEX_VOL_M2: a volume slab layered along a main axis (x- or
+// y-layers, forward.cu's main-axis kernel; M2 when nx != ny).
+enum TexRole { TEX_VOLUME = 0, TEX_PROJ = 1, TEX_VOL_M = 2, TEX_VOL_M2 = 3 };
+
+// Main axis of a view (0 = x, 1 = y): the larger |x| / |y| component of the
+// central ray.  Host side.
+inline int view_axis(const double* g12, int n_u, int n_v) {
+  double d[2];
+  for (int i = 0; i < 2; i++)
+    d[i] = g12[3 + i] + 0.5 * (n_u - 1) * g12[6 + i] +
+           0.5 * (n_v - 1) * g12[9 + i] - g12[i];
+  return fabs(d[0]) >= fabs(d[1]) ? 0 : 1;
+}
 
 // Cached (w, h, >= layers) surface-writable layered array, contents
 // undefined; stream-ordered reuse per (device, stream, role).
+// taller_ok: an array of height >= h may be reused (the caller zeroes the
+// rows past h that its reads can reach).
 int acquire_layered(TexRole role, int w, int h, int layers, cudaStream_t s,
-                    LayeredTexture** out);
+                    LayeredTexture** out, bool taller_ok = false);
 
 // Returns a texture whose array is (w, h, >= layers) and loads `layers`
 // layers from the linear array `src` ([layers][h][w], device or host
@@ -277,6 +302,8 @@ int load_layered(TexRole role, const float* src, int w, int h, int layers,
 
 // Max layers of a 2D layered texture on this device (2048 on sm_100).
 int max_layers();
+// Max width / height of a 2D layered texture on this device.
+int max_layered_height();
 
 // Default mempool keeps freed memory (see runtime.cu).
 void retain_pool();

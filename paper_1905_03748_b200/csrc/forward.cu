@@ -104,6 +104,218 @@ __global__ void __launch_bounds__(128, FWD_MINB)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K1 on main-axis layers.  For views whose central ray runs mainly along
+// M (x or y), the slab is held as a 2D-layered texture with one layer per
+// M plane (texel (T, z - s0) of layer iM), and a warp's quads are 4
+// v-ADJACENT rays: rays of one detector column share their xy path and,
+// with equal sample counts, their x / y sample positions, so their cells
+// change together -- the texture pipe charges a tld4 per quad with any
+// active lane.  An M-advance by one plane re-gathers one layer (the other
+// is the previous far layer); a T or z change re-gathers both.  T and z
+// outside the texture read the border zero (the reference's padding and
+// the slab's z range); layers are masked in the weights.
+#ifndef FWD_ML_MINB
+#define FWD_ML_MINB 10  // 48 registers, no spills: 40 warps/SM hide the tld4 latency
+#endif
+template <int MODE, int M>
+__global__ void __launch_bounds__(128, FWD_ML_MINB)
+    fwd_mlayer_kernel(cudaTextureObject_t tex,
+                      const AngleGeom* __restrict__ geom,
+                      const int* __restrict__ view_ids, Grid G,
+                      double step_max, int z_lo, int z_hi, int n_u, int n_v,
+                      int v_base, int v_end, float* __restrict__ out,
+                      const float* __restrict__ b,
+                      const float* __restrict__ w) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int u = blockIdx.x * FWD_TILE_U + (warp & 1) * 8 + (lane >> 2);
+  const int v = v_base + blockIdx.y * FWD_TILE_V + (warp >> 1) * 4 + (lane & 3);
+  const int a = view_ids[blockIdx.z];
+  if (u >= n_u || v >= v_end) return;
+  Ray r;
+  setup_ray(geom[a], G, step_max, u, v, r);
+  float acc = 0.f;
+  if (r.n > 0) {
+    March m;
+    march_params(r, G, m);
+    long long k0l, k1l;
+    slab_k_range(r, m, G, z_lo, z_hi, k0l, k1l);
+    const int k0 = (int)k0l, k1 = (int)k1l;
+    constexpr int T = 1 - M;
+    const int top = G.n[M] - 1;
+    long long qm = q_at(m, k0, M), qt = q_at(m, k0, T), qz = q_at(m, k0, 2);
+    const long long bm = m.Bq[M], bt = m.Bq[T], bz = m.Bq[2];
+    // Software-pipelined: the gathers of sample k + 1 are issued before
+    // sample k is interpolated -- with the quads skipping together the
+    // texture pipe is no longer saturated and the kernel is tld4-latency
+    // bound (r01 A/B at config 2, 90-view launches incl. texture fills:
+    // re-gather on change 283 GUPS; one-layer M-step reuse through
+    // predicated gathers 242 (+38% instructions); pipelined 309; pipelined
+    // at 48 registers / 40 warps per SM 325; at 40 registers (spills) 310).
+    int cm = q_cell(qm), ct = q_cell(qt), cz = q_cell(qz);
+    float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, n0 = s0, n1 = s0;
+    if (k0 < k1) {
+      const float tx = int_to_float(ct + 1), ty = int_to_float(cz - z_lo + 1);
+      s0 = gather_a2d(tex, cm, tx, ty);
+      s1 = gather_a2d(tex, cm + 1, tx, ty);
+    }
+#pragma unroll 1
+    for (int k = k0; k < k1; ++k) {
+      const float wm = q_frac(qm), wt = q_frac(qt), wz = q_frac(qz);
+      const float m0 = (cm >= 0 && cm <= top) ? 1.f - wm : 0.f;
+      const float m1 = (cm + 1 >= 0 && cm + 1 <= top) ? wm : 0.f;
+      qm += bm;
+      qt += bt;
+      qz += bz;
+      const int im = q_cell(qm), it = q_cell(qt), iz = q_cell(qz);
+      const bool ch = im != cm || it != ct || iz != cz;
+      {
+        const float tx = int_to_float(it + 1);
+        const float ty = int_to_float(iz - z_lo + 1);
+        gather_a2d_if(n0, ch, tex, im, tx, ty);
+        gather_a2d_if(n1, ch, tex, im + 1, tx, ty);
+      }
+      const float r00 = fmaf(wt, s0.z - s0.w, s0.w);
+      const float r01 = fmaf(wt, s0.y - s0.x, s0.x);
+      const float r10 = fmaf(wt, s1.z - s1.w, s1.w);
+      const float r11 = fmaf(wt, s1.y - s1.x, s1.x);
+      const float b0 = fmaf(wz, r01 - r00, r00);
+      const float b1 = fmaf(wz, r11 - r10, r10);
+      acc = fmaf(m0, b0, fmaf(m1, b1, acc));
+      if (ch) {
+        s0 = n0;
+        s1 = n1;
+      }
+      cm = im;
+      ct = it;
+      cz = iz;
+    }
+  }
+  const float val = acc * (float)r.step;
+  const size_t idx = ((size_t)a * n_v + v) * n_u + u;
+  if (MODE == FWD_OVERWRITE) {
+    out[idx] = val;
+  } else if (MODE == FWD_ACCUMULATE) {
+    out[idx] += val;
+  } else {
+    const float wt = w ? w[idx] : 1.f;
+    out[idx] = wt * (b[idx] - val);
+  }
+}
+
+// Slab [nzs, ny, nx] -> x-layers (layer x, texel (y, z)): 32x32 (x, y)
+// tiles transposed through shared memory so both the volume reads and the
+// surface writes are row-contiguous.
+// Grid z extent > nzs: rows z >= nzs are written as zeros (guard rows of
+// an array taller than the slab).
+__global__ void fill_xlayers_kernel(cudaSurfaceObject_t surf,
+                                    const float* __restrict__ vol, int nx,
+                                    int ny, int nzs) {
+  __shared__ float tile[32][33];
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32, z = blockIdx.z;
+  const size_t plane = (size_t)nx * ny;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int x = x0 + threadIdx.x, y = y0 + j;
+    tile[j][threadIdx.x] =
+        (x < nx && y < ny && z < nzs)
+            ? vol[(size_t)z * plane + (size_t)y * nx + x] : 0.f;
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int x = x0 + j, y = y0 + threadIdx.x;
+    if (x < nx && y < ny)
+      surf2DLayeredwrite(tile[threadIdx.x][j], surf, y * (int)sizeof(float), z,
+                         x);
+  }
+}
+
+// Slab [nzs, ny, nx] -> y-layers (layer y, texel (x, z)).
+__global__ void fill_ylayers_kernel(cudaSurfaceObject_t surf,
+                                    const float* __restrict__ vol, int nx,
+                                    int ny, int nzs) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x < nx)
+    surf2DLayeredwrite(z < nzs ? vol[((size_t)z * ny + y) * nx + x] : 0.f,
+                       surf, x * (int)sizeof(float), z, y);
+}
+
+// Loads slab planes [0, nzs) of `vol` as main-axis-M layers.
+static int load_mlayers(int M, const float* vol, int nx, int ny, int nzs,
+                        cudaStream_t s, LayeredTexture** t) {
+  const TexRole role = (M == 1 && nx != ny) ? TEX_VOL_M2 : TEX_VOL_M;
+  // slabs of different heights reuse a taller array (no reallocation and
+  // stream drain per slab)
+  int rc = M == 0 ? acquire_layered(role, ny, nzs, nx, s, t, true)
+                  : acquire_layered(role, nx, nzs, ny, s, t, true);
+  if (rc) return rc;
+  // rows past the slab must read zero: slab_k_range keeps <= 3 samples
+  // beyond the slab (<= 1.5 planes at |dz| <= 1/2 voxel per sample), so a
+  // taller array gets 4 zero guard rows
+  const int zr = min((*t)->h, nzs + 4);
+  if (M == 0) {
+    fill_xlayers_kernel<<<dim3((nx + 31) / 32, (ny + 31) / 32, zr),
+                          dim3(32, 8), 0, s>>>((*t)->surf, vol, nx, ny, nzs);
+  } else {
+    fill_ylayers_kernel<<<dim3((nx + 127) / 128, ny, zr), 128, 0, s>>>(
+        (*t)->surf, vol, nx, ny, nzs);
+  }
+  CS_COUNT_LAUNCH();
+  CS_CHECK_CUDA(cudaGetLastError());
+  return CS_OK;
+}
+
+// Main-axis-layered K1 over all n_a views: views grouped by main axis, one
+// texture fill + one launch per group (the two fills share one array when
+// nx == ny; stream order separates them).  Slab height and the layer
+// counts nx, ny must fit the layered-texture limits (caller checks).
+template <int MODE>
+static int launch_mlayer(const float* vol, int nx, int ny, int nz, int z_lo,
+                         int z_hi, const Grid& G, const double* geom,
+                         const AngleGeom* dgeom, int n_a, int n_u, int n_v,
+                         double step_max, float* out, const float* b,
+                         const float* w, cudaStream_t s) {
+  int* ids_h = (int*)malloc(sizeof(int) * (size_t)n_a);
+  int cnt[2] = {0, 0}, m = 0;
+  for (int c = 0; c < 2; c++)
+    for (int a = 0; a < n_a; a++)
+      if (view_axis(geom + 12 * a, n_u, n_v) == c) {
+        ids_h[m++] = a;
+        cnt[c]++;
+      }
+  int* ids = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&ids, sizeof(int) * n_a, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(ids, ids_h, sizeof(int) * n_a, cudaMemcpyHostToDevice,
+                        s);
+  // the host table must outlive the async copy: it is pageable, so the copy
+  // is staged before cudaMemcpyAsync returns
+  free(ids_h);
+  CS_CHECK_CUDA(e);
+  int rc = CS_OK;
+  int v0 = 0, v1 = n_v;
+  if (MODE != FWD_RESIDUAL && cull_enabled())
+    slab_row_band(geom, n_a, G, z_lo, z_hi, n_v, &v0, &v1);
+  if (MODE == FWD_OVERWRITE)
+    rc = zero_rows_outside(out, n_a, n_u, n_v, v0, v1, s);
+  for (int c = 0; c < 2 && rc == CS_OK && v1 > v0; c++) {
+    if (!cnt[c]) continue;
+    LayeredTexture* t = nullptr;
+    if ((rc = load_mlayers(c, vol, nx, ny, z_hi - z_lo, s, &t))) break;
+    const dim3 grid((n_u + FWD_TILE_U - 1) / FWD_TILE_U,
+                    (v1 - v0 + FWD_TILE_V - 1) / FWD_TILE_V, cnt[c]);
+    auto kern = c == 0 ? fwd_mlayer_kernel<MODE, 0> : fwd_mlayer_kernel<MODE, 1>;
+    kern<<<grid, 128, 0, s>>>(t->tex, dgeom, ids + (c ? cnt[0] : 0), G,
+                              step_max, z_lo, z_hi, n_u, n_v, v0, v1, out, b,
+                              w);
+    CS_COUNT_LAUNCH();
+    if ((e = cudaGetLastError()) != cudaSuccess) break;
+  }
+  cudaFreeAsync(ids, s);
+  CS_CHECK_CUDA(e);
+  return rc;
+}
+
 // Siddon traversal, _kernels.py:71-151 (fp64, midpoint attribution).
 #ifndef SID_MINB
 #define SID_MINB 10  // <= 48 registers: 40 warps/SM hide the fp64 chain latency
@@ -215,6 +427,16 @@ static int launch_interp(const float* vol, int nx, int ny, int nz, int z_lo,
   AngleGeom* dgeom = nullptr;
   if ((rc = upload_geometry(geom, n_a, s, &dgeom))) return rc;
   const int maxl = max_layers();
+  // main-axis-layered kernel unless disabled (CS_FWD_MLAYER=0) or the
+  // x / y extents exceed the layer limit (then z-layers, sub-slabbed)
+  static const char* ml_knob = getenv("CS_FWD_MLAYER");
+  if (!(ml_knob && ml_knob[0] == '0') && nx <= maxl && ny <= maxl &&
+      z_hi - z_lo <= max_layered_height()) {
+    rc = launch_mlayer<MODE>(vol, nx, ny, nz, z_lo, z_hi, G, geom, dgeom, n_a,
+                             n_u, n_v, step_max, out, b, w, s);
+    release_geometry(dgeom, s);
+    return rc;
+  }
   // Slabs taller than the layer limit go through in sub-slabs;
   // the first sub-slab applies MODE, the rest accumulate.
   const dim3 block(128);

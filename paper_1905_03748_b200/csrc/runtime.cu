@@ -33,6 +33,22 @@ Grid make_grid(const double grid6[6], int nx, int ny, int nz) {
   return G;
 }
 
+int max_layered_height() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0, h = 0, w = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&h, cudaDevAttrMaxTexture2DLayeredHeight,
+                               dev) != cudaSuccess)
+      h = 16384;
+    if (cudaDeviceGetAttribute(&w, cudaDevAttrMaxTexture2DLayeredWidth,
+                               dev) != cudaSuccess)
+      w = 16384;
+    v = h < w ? h : w;
+  }
+  return v;
+}
+
 int max_layers() {
   static int v = -1;
   if (v < 0) {
@@ -88,7 +104,7 @@ int make_texture(LayeredTexture& t, int w, int h, int layers) {
 }  // namespace
 
 int acquire_layered(TexRole role, int w, int h, int layers, cudaStream_t s,
-                    LayeredTexture** out) {
+                    LayeredTexture** out, bool taller_ok) {
   CS_REQUIRE(layers >= 1 && layers <= max_layers(), CS_ERR_ARG,
              "layered texture: %d layers outside [1, %d]", layers,
              max_layers());
@@ -96,7 +112,8 @@ int acquire_layered(TexRole role, int w, int h, int layers, cudaStream_t s,
   CS_CHECK_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(g_mu);
   LayeredTexture& t = g_cache[Key{dev, s, (int)role}];
-  if (t.array && (t.w != w || t.h != h || t.layers < layers)) {
+  if (t.array && (t.w != w || (taller_ok ? t.h < h : t.h != h) ||
+                  t.layers < layers)) {
     // shape change: previous launches on this stream may still read the old
     // array, so drain the stream before releasing it.
     CS_CHECK_CUDA(cudaStreamSynchronize(s));

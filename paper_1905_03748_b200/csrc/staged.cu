@@ -485,21 +485,6 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
   }
 }
 
-// Main axis of a view from its central ray: 0 = x, 1 = y.
-static int view_axis(const double* g12, int n_u, int n_v) {
-  double d[2];
-  for (int i = 0; i < 2; i++)
-    d[i] = g12[3 + i] + 0.5 * (n_u - 1) * g12[6 + i] +
-           0.5 * (n_v - 1) * g12[9 + i] - g12[i];
-  return fabs(d[0]) >= fabs(d[1]) ? 0 : 1;
-}
-
-// Fixed-point budget for matched deposits: the int32 box must hold the
-// largest per-voxel chunk sum.  A voxel's trilinear support (2 voxels per
-// axis) is crossed by at most (2 / footprint + 1)^2 rays and each ray puts
-// at most (2 / min step + 1) samples of weight <= 1 into it; the footprint
-// of a pixel is smallest nearest the source (magnification dsd / (dso - r)).
-// Returns the scale numerator: per CTA, scale = budget / max|val * step|.
 // Smallest footprint of a detector pixel on the grid, in voxels (pixels
 // nearest the source are smallest: magnification dsd / (dso - r)).
 static double min_pixel_footprint(const double* grid6, int nx, int ny,
@@ -529,6 +514,12 @@ static double min_pixel_footprint(const double* grid6, int nx, int ny,
   return fp;
 }
 
+// Fixed-point budget for matched deposits: the int32 box must hold the
+// largest per-voxel chunk sum.  A voxel's trilinear support (2 voxels per
+// axis) is crossed by at most (2 / footprint + 1)^2 rays and each ray puts
+// at most (2 / min step + 1) samples of weight <= 1 into it; the footprint
+// of a pixel is smallest nearest the source (magnification dsd / (dso - r)).
+// Returns the scale numerator: per CTA, scale = budget / max|val * step|.
 static float fixed_point_budget(const double* grid6, int nx, int ny, int nz,
                                 const double* geom, int n_a, int n_u, int n_v,
                                 double step_max) {

@@ -538,3 +538,57 @@ def test_fine_detector_lane_strides_subprocess():
         r = subprocess.run([sys.executable, "-c", code], env=env,
                            capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, (s, r.stderr[-2000:])
+
+
+def test_ax_texture_reuse_across_slab_heights():
+    """The main-axis-layered Ax reuses a taller texture array for shorter
+    slabs (rows past the slab are zeroed guard rows): a tall launch followed
+    by short slab launches near the top / bottom / middle, each against
+    the oracle; views of both main axes and a non-cubic grid (x- and
+    y-layered arrays differ)."""
+    for dims in ((20, 20, 24), (22, 18, 24)):
+        nx, ny, nz = dims
+        g = _odd_geometry(nx, ny, nz, 30, 28, 8)
+        og = to_oracle(g)
+        x = np.random.default_rng(17).random((nz, ny, nx), dtype=np.float32) + 0.5
+        full = cs.forward_project_slab(cs.Volume(g.voxel_grid, x), g, (0, 8),
+                                       IP).data
+        assert rel_l2(full, O.fwd_interp(x, og)) <= TOL_OP
+        for zr in ((nz - 3, nz), (0, 2), (9, 14), (5, 21)):
+            xs = x[zr[0]:zr[1]]
+            got = cs.forward_project_slab(cs.Volume(g.voxel_grid, xs, zr), g,
+                                          (0, 8), IP).data
+            assert rel_l2(got, O.fwd_interp(xs, og, (0, 8), zr)) <= TOL_OP, zr
+
+
+def test_ax_z_layered_fallback_subprocess():
+    """The z-layered Ax (used when nx or ny exceeds the layered-texture
+    limit; forced here with CS_FWD_MLAYER=0, read once, hence a
+    subprocess): full volume, slabs and the residual epilogue against the
+    oracle."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path[:0] = [%r, %r]\n"
+        "import numpy as np, torch, paper_1905_03748_b200 as cs\n"
+        "from paper_1905_03748_b200 import kernels as K\n"
+        "from conftest import to_oracle, rel_l2\n"
+        "from oracle import oracle as O\n"
+        "from test_gpu_parity import _odd_geometry\n"
+        "g = _odd_geometry(30, 26, 21, 33, 19, 11)\n"
+        "og = to_oracle(g)\n"
+        "x = np.random.default_rng(3).random((21, 26, 30), dtype=np.float32)\n"
+        "IP = cs.ProjectionMethod.INTERPOLATED\n"
+        "got = cs.forward_project_slab(cs.Volume(g.voxel_grid, x), g, (0, 11), IP).data\n"
+        "e1 = rel_l2(got, O.fwd_interp(x, og))\n"
+        "xs = x[4:15]\n"
+        "got = cs.forward_project_slab(cs.Volume(g.voxel_grid, xs, (4, 15)), g, (2, 9), IP).data\n"
+        "e2 = rel_l2(got, O.fwd_interp(xs, og, (2, 9), (4, 15)))\n"
+        "print(e1, e2); assert e1 <= 1e-5 and e2 <= 1e-5\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+         os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CS_FWD_MLAYER="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
