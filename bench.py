@@ -379,7 +379,9 @@ def run_ours(args):
         kname, kt, kupd = ("bwd_matched_kernel", t_atb / len(atb_chunks),
                            upd_atb / len(atb_chunks))
     else:
-        kname, kt, kupd = ("fwd_interp_kernel", t_ax / len(ax_chunks),
+        # main-axis-layered Ax (z-layered only past the layer limit)
+        kname = ("fwd_mlayer_kernel" if n <= 2048 else "fwd_interp_kernel")
+        kname, kt, kupd = (kname, t_ax / len(ax_chunks),
                            upd_ax / len(ax_chunks))
     peak, peak_kind = measured_peak()
     achieved = kupd * bpu / kt / 1e9

@@ -29,7 +29,12 @@ METRICS = [
     ("launch__registers_per_thread", "regs"),
     ("smsp__inst_executed.sum", "warp insts"),
 ]
-KEYS = {"fwd_interp": "fwd_interp_kernel",
+# kernel-name fragment -> bench key.  One Ax call on main-axis layers is
+# fill_xlayers + fwd_mlayer<.., 0> + fill_ylayers + fwd_mlayer<.., 1>: the
+# fills count in its DRAM traffic, only the projector in its pipe limits.
+KEYS = {"fwd_mlayer": "fwd_mlayer_kernel", "fill_xlayers": "fwd_mlayer_kernel",
+        "fill_ylayers": "fwd_mlayer_kernel",
+        "fwd_interp": "fwd_interp_kernel",
         "staged_kernel<1": "bwd_matched_kernel",
         "bwd_fdk": "bwd_fdk_kernel", "fdk_staged": "bwd_fdk_kernel",
         "fwd_siddon": "fwd_siddon_kernel"}
@@ -84,7 +89,7 @@ def main():
         limits = {}
     for rec in rows_out:
         for k, key in KEYS.items():
-            if k not in rec["kernel"]:
+            if k not in rec["kernel"] or k.startswith("fill_"):
                 continue
             ent = {}
             for label in ("TEX writeback %", "issue active %", "L1/TEX thru %",

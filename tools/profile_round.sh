@@ -9,5 +9,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/$T/launches.csv python bench.py --steps 2 --warmup 3 --no-extras \
   > gpurun_out/$T/launches_bench.log 2>&1
 PROF_KERNELS=fwd,matched,fdk timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"fwd_interp|staged" -s 4 -c 4 -o gpurun_out/$T/full python tools/prof_c2.py \
+  -k regex:"fwd_mlayer|fill_|staged" -s 7 -c 7 -o gpurun_out/$T/full python tools/prof_c2.py \
   > gpurun_out/$T/ncu_full.log 2>&1
