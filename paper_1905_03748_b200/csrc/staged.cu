@@ -368,15 +368,21 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
     }
     // ---- samples of the chunk
     if (any) {
-      // exact fixed-point positions (common.cuh), integer-advanced
+      // exact fixed-point positions (common.cuh), integer-advanced; on the
+      // staged path relative to the box origin (an exact integer shift), so
+      // the cells index the box directly
       long long qx = q_at(m, ka, 0), qy = q_at(m, ka, 1), qz = q_at(m, ka, 2);
+      if (fits) {
+        qx -= (long long)bo[0] << QF;
+        qy -= (long long)bo[1] << QF;
+        qz -= (long long)bo[2] << QF;
+      }
       for (int kk = ka; kk < kb;
            kk++, qx += m.Bq[0], qy += m.Bq[1], qz += m.Bq[2]) {
         const float wx = q_frac(qx), wy = q_frac(qy), wz = q_frac(qz);
         const int ix = q_cell(qx), iy = q_cell(qy), iz = q_cell(qz);
         if (fits) {
-          const int b = (iz - bo[2]) * sz + (iy - bo[1]) * sy +
-                        (ix - bo[0]) * sx;
+          const int b = iz * sz + iy * sy + ix * sx;
           if (OP == OP_FWD) {
             const float s000 = st_box[b], s001 = st_box[b + sx];
             const float s010 = st_box[b + sy], s011 = st_box[b + sy + sx];
