@@ -203,41 +203,47 @@ __global__ void __launch_bounds__(128, FWD_ML_MINB)
   }
 }
 
-// Slab [nzs, ny, nx] -> x-layers (layer x, texel (y, z)): 32x32 (x, y)
-// tiles transposed through shared memory so both the volume reads and the
-// surface writes are row-contiguous.
-// Grid z extent > nzs: rows z >= nzs are written as zeros (guard rows of
-// an array taller than the slab).
-__global__ void fill_xlayers_kernel(cudaSurfaceObject_t surf,
-                                    const float* __restrict__ vol, int nx,
-                                    int ny, int nzs) {
-  __shared__ float tile[32][33];
-  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32, z = blockIdx.z;
+// Slab [nzs, ny, nx] -> x-layers (layer x, texel (y, z)).  A CTA moves a
+// 32 x 32 y x 8 z brick through shared memory: row-contiguous volume reads,
+// and per layer a 32 y x 8 z surface block (two whole 64 B x 8-row GOBs of
+// the block-linear array).  Rows z in [nzs, zr) are written as zeros (guard
+// rows of an array taller than the slab).
+__global__ void __launch_bounds__(256)
+    fill_xlayers_kernel(cudaSurfaceObject_t surf,
+                        const float* __restrict__ vol, int nx, int ny, int nzs,
+                        int zr) {
+  __shared__ float brick[8][32][33];
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32, z0 = blockIdx.z * 8;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
   const size_t plane = (size_t)nx * ny;
-  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
-    const int x = x0 + threadIdx.x, y = y0 + j;
-    tile[j][threadIdx.x] =
-        (x < nx && y < ny && z < nzs)
-            ? vol[(size_t)z * plane + (size_t)y * nx + x] : 0.f;
+  for (int zz = 0; zz < 8; zz++) {
+    const int z = z0 + zz;
+    for (int j = ty; j < 32; j += 8) {
+      const int x = x0 + tx, y = y0 + j;
+      brick[zz][j][tx] = (x < nx && y < ny && z < nzs)
+                             ? vol[(size_t)z * plane + (size_t)y * nx + x]
+                             : 0.f;
+    }
   }
   __syncthreads();
-  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
-    const int x = x0 + j, y = y0 + threadIdx.x;
-    if (x < nx && y < ny)
-      surf2DLayeredwrite(tile[threadIdx.x][j], surf, y * (int)sizeof(float), z,
-                         x);
-  }
+  const int z = z0 + ty, y = y0 + tx;
+  if (z >= zr || y >= ny) return;
+  for (int j = 0; j < 32 && x0 + j < nx; j++)
+    surf2DLayeredwrite(brick[ty][tx][j], surf, y * (int)sizeof(float), z,
+                       x0 + j);
 }
 
-// Slab [nzs, ny, nx] -> y-layers (layer y, texel (x, z)).
-__global__ void fill_ylayers_kernel(cudaSurfaceObject_t surf,
-                                    const float* __restrict__ vol, int nx,
-                                    int ny, int nzs) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
-  if (x < nx)
-    surf2DLayeredwrite(z < nzs ? vol[((size_t)z * ny + y) * nx + x] : 0.f,
-                       surf, x * (int)sizeof(float), z, y);
+// Slab [nzs, ny, nx] -> y-layers (layer y, texel (x, z)): a CTA writes a
+// 32 x x 8 z block of one layer (two whole GOBs), reading 8 row segments.
+__global__ void __launch_bounds__(256)
+    fill_ylayers_kernel(cudaSurfaceObject_t surf,
+                        const float* __restrict__ vol, int nx, int ny, int nzs,
+                        int zr) {
+  const int x = blockIdx.x * 32 + threadIdx.x;
+  const int z = blockIdx.y * 8 + threadIdx.y, y = blockIdx.z;
+  if (x >= nx || z >= zr) return;
+  surf2DLayeredwrite(z < nzs ? vol[((size_t)z * ny + y) * nx + x] : 0.f, surf,
+                     x * (int)sizeof(float), z, y);
 }
 
 // Loads slab planes [0, nzs) of `vol` as main-axis-M layers.
@@ -254,11 +260,12 @@ static int load_mlayers(int M, const float* vol, int nx, int ny, int nzs,
   // taller array gets 4 zero guard rows
   const int zr = min((*t)->h, nzs + 4);
   if (M == 0) {
-    fill_xlayers_kernel<<<dim3((nx + 31) / 32, (ny + 31) / 32, zr),
-                          dim3(32, 8), 0, s>>>((*t)->surf, vol, nx, ny, nzs);
+    fill_xlayers_kernel<<<dim3((nx + 31) / 32, (ny + 31) / 32, (zr + 7) / 8),
+                          dim3(32, 8), 0, s>>>((*t)->surf, vol, nx, ny, nzs,
+                                               zr);
   } else {
-    fill_ylayers_kernel<<<dim3((nx + 127) / 128, ny, zr), 128, 0, s>>>(
-        (*t)->surf, vol, nx, ny, nzs);
+    fill_ylayers_kernel<<<dim3((nx + 31) / 32, (zr + 7) / 8, ny), dim3(32, 8),
+                          0, s>>>((*t)->surf, vol, nx, ny, nzs, zr);
   }
   CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
