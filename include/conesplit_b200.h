@@ -48,6 +48,11 @@ const char* cs_last_error(void);
 long long cs_launch_count(void);
 /* Blocks the host until `stream` drains (the only synchronising call). */
 int cs_sync(cs_stream_t stream);
+/* Frees the library's cached texture arrays on the current device (one per
+ * stream and layout, each the size of the largest slab / stack projected
+ * through it); synchronises the device first.  Called by the Python layer
+ * before retrying a call that ran out of device memory. */
+int cs_release_cache(void);
 
 /* ---------------------------------------------------------------- Ax ---- */
 

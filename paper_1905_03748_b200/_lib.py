@@ -39,6 +39,7 @@ SYMBOLS: dict[str, list] = {
     "cs_last_error": [],
     "cs_sync": [P],
     "cs_launch_count": [],
+    "cs_release_cache": [],
     "cs_fwd_interp": [P, I, I, I, I, I, P, P, I, I, I, D, P, I, P],
     "cs_fwd_interp_residual": [P, I, I, I, P, P, I, I, I, D, P, P, P, P],
     "cs_fwd_siddon": [P, I, I, I, I, I, P, P, I, I, I, P, I, P],

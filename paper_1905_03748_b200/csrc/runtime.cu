@@ -262,4 +262,25 @@ int cs_sync(cs_stream_t stream) {
   return CS_OK;
 }
 
+int cs_release_cache(void) {
+  int dev = 0;
+  CS_CHECK_CUDA(cudaGetDevice(&dev));
+  // texture reads of queued launches must finish before their arrays go
+  CS_CHECK_CUDA(cudaDeviceSynchronize());
+  std::lock_guard<std::mutex> lock(cs::g_mu);
+  for (auto it = cs::g_cache.begin(); it != cs::g_cache.end();) {
+    if (it->first.device != dev) {
+      ++it;
+      continue;
+    }
+    cs::LayeredTexture& t = it->second;
+    if (t.surf) cudaDestroySurfaceObject(t.surf);
+    if (t.tex) cudaDestroyTextureObject(t.tex);
+    if (t.array) cudaFreeArray(t.array);
+    it = cs::g_cache.erase(it);
+  }
+  CS_CHECK_CUDA(cudaGetLastError());
+  return CS_OK;
+}
+
 }  // extern "C"

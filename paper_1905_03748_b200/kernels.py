@@ -20,16 +20,23 @@ MAX_ANGLES_PER_LAUNCH = 65535  # grid.z limit of the ray kernels
 def _checked_retry_oom(call):
     """check(call()); if the library ran out of device memory (its texture
     arrays and stream-ordered tables are allocated outside torch), release
-    torch's cached blocks and retry once.  The C-ABI allocates before it
-    launches anything, so a failed call left no partial result."""
+    torch's cached blocks and the library's cached texture arrays, then
+    retry once.  The C-ABI allocates before it launches anything, so a
+    failed call left no partial result."""
     rc = call()
     if rc != 0:
         msg = lib().cs_last_error().decode()
         if "out of memory" in msg:
             torch.cuda.synchronize()
             torch.cuda.empty_cache()
+            check(lib().cs_release_cache())
             rc = call()
     check(rc)
+
+
+def release_cache() -> None:
+    """Free the library's cached texture arrays on the current device."""
+    check(lib().cs_release_cache())
 
 
 def launch_count() -> int:

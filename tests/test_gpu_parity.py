@@ -592,3 +592,19 @@ def test_ax_z_layered_fallback_subprocess():
     r = subprocess.run([sys.executable, "-c", code], env=env,
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+def test_release_cache_then_reuse():
+    """cs_release_cache frees the cached texture arrays; the next calls
+    re-create them and give identical results."""
+    from paper_1905_03748_b200 import kernels as K
+    import torch
+    g = _odd_geometry(16, 14, 12, 20, 18, 6)
+    x = torch.rand((12, 14, 16), device="cuda")
+    p1 = torch.empty((6, 18, 20), device="cuda")
+    K.fwd_interp(x, g, (0, 6), (0, 12), p1)
+    K.release_cache()
+    p2 = torch.empty_like(p1)
+    K.fwd_interp(x, g, (0, 6), (0, 12), p2)
+    assert torch.equal(p1, p2)
+    K.release_cache()
