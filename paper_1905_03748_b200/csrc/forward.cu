@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(128, FWD_MINB)
 // outside the texture read the border zero (the reference's padding and
 // the slab's z range); layers are masked in the weights.
 #ifndef FWD_ML_MINB
-#define FWD_ML_MINB 10  // 48 registers, no spills: 40 warps/SM hide the tld4 latency
+#define FWD_ML_MINB 8  // 64 registers (two prefetch buffers), 32 warps/SM
 #endif
 template <int MODE, int M>
 __global__ void __launch_bounds__(128, FWD_ML_MINB)
@@ -148,19 +148,27 @@ __global__ void __launch_bounds__(128, FWD_ML_MINB)
     // Software-pipelined: the gathers of sample k + 1 are issued before
     // sample k is interpolated -- with the quads skipping together the
     // texture pipe is no longer saturated and the kernel is tld4-latency
-    // bound (r01 A/B at config 2, 90-view launches incl. texture fills:
+    // bound.  r01 A/B at config 2 (90-view launches incl. texture fills):
     // re-gather on change 283 GUPS; one-layer M-step reuse through
-    // predicated gathers 242 (+38% instructions); pipelined 309; pipelined
-    // at 48 registers / 40 warps per SM 325; at 40 registers (spills) 310).
+    // predicated gathers 242 (+38% instructions); one prefetch buffer 309
+    // (56 regs) / 325 (48 regs, 40 warps/SM) -- its rotation waited on the
+    // gathers just issued; two buffers (below) 344 (64 regs) / 326 (56) /
+    // 283 (48, spills).
+    // Two prefetch buffers: sample k+1's gathers go to one while sample
+    // k's data is taken from the other (gathered one iteration earlier), so
+    // the wait for a gather spans a whole iteration.
     int cm = q_cell(qm), ct = q_cell(qt), cz = q_cell(qz);
-    float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, n0 = s0, n1 = s0;
+    const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 s0 = zero4, s1 = zero4, pa0 = zero4, pa1 = zero4, pb0 = zero4,
+           pb1 = zero4;
+    bool chk = true;
     if (k0 < k1) {
       const float tx = int_to_float(ct + 1), ty = int_to_float(cz - z_lo + 1);
-      s0 = gather_a2d(tex, cm, tx, ty);
-      s1 = gather_a2d(tex, cm + 1, tx, ty);
+      pb0 = gather_a2d(tex, cm, tx, ty);
+      pb1 = gather_a2d(tex, cm + 1, tx, ty);
     }
-#pragma unroll 1
-    for (int k = k0; k < k1; ++k) {
+    auto body = [&](float4& n0, float4& n1, const float4& p0,
+                    const float4& p1) {
       const float wm = q_frac(qm), wt = q_frac(qt), wz = q_frac(qz);
       const float m0 = (cm >= 0 && cm <= top) ? 1.f - wm : 0.f;
       const float m1 = (cm + 1 >= 0 && cm + 1 <= top) ? wm : 0.f;
@@ -175,6 +183,10 @@ __global__ void __launch_bounds__(128, FWD_ML_MINB)
         gather_a2d_if(n0, ch, tex, im, tx, ty);
         gather_a2d_if(n1, ch, tex, im + 1, tx, ty);
       }
+      if (chk) {
+        s0 = p0;
+        s1 = p1;
+      }
       const float r00 = fmaf(wt, s0.z - s0.w, s0.w);
       const float r01 = fmaf(wt, s0.y - s0.x, s0.x);
       const float r10 = fmaf(wt, s1.z - s1.w, s1.w);
@@ -182,14 +194,18 @@ __global__ void __launch_bounds__(128, FWD_ML_MINB)
       const float b0 = fmaf(wz, r01 - r00, r00);
       const float b1 = fmaf(wz, r11 - r10, r10);
       acc = fmaf(m0, b0, fmaf(m1, b1, acc));
-      if (ch) {
-        s0 = n0;
-        s1 = n1;
-      }
+      chk = ch;
       cm = im;
       ct = it;
       cz = iz;
+    };
+    int k = k0;
+#pragma unroll 1
+    for (; k + 1 < k1; k += 2) {
+      body(pa0, pa1, pb0, pb1);
+      body(pb0, pb1, pa0, pa1);
     }
+    if (k < k1) body(pa0, pa1, pb0, pb1);
   }
   const float val = acc * (float)r.step;
   const size_t idx = ((size_t)a * n_v + v) * n_u + u;
