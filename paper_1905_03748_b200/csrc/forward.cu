@@ -16,6 +16,7 @@
 // slab launch costs only its share of the ray.
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -429,6 +430,33 @@ static int check_common(int nx, int ny, int nz, int z_lo, int z_hi, int n_a,
   return CS_OK;
 }
 
+// One z-layered K1 pass over the sub-slab [z_lo, z_hi) (nzs <= layer limit).
+template <int MODE>
+static int launch_zlayer(const float* vol, int nx, int ny, int nz, int z_lo,
+                         int z_hi, const Grid& G, const double* geom,
+                         const AngleGeom* dgeom, int n_a, int n_u, int n_v,
+                         double step_max, float* out, const float* b,
+                         const float* w, cudaStream_t s) {
+  int v0 = 0, v1 = n_v, rc;
+  if (MODE != FWD_RESIDUAL && cull_enabled())
+    slab_row_band(geom, n_a, G, z_lo, z_hi, n_v, &v0, &v1);
+  if (MODE == FWD_OVERWRITE &&
+      (rc = zero_rows_outside(out, n_a, n_u, n_v, v0, v1, s)))
+    return rc;
+  if (v1 <= v0) return CS_OK;
+  LayeredTexture* t = nullptr;
+  if ((rc = load_layered(TEX_VOLUME, vol, nx, ny, z_hi - z_lo, s, &t)))
+    return rc;
+  const dim3 grid((n_u + FWD_TILE_U - 1) / FWD_TILE_U,
+                  (v1 - v0 + FWD_TILE_V - 1) / FWD_TILE_V, n_a);
+  fwd_interp_kernel<MODE><<<grid, 128, 0, s>>>(t->tex, dgeom, G, step_max,
+                                               z_lo, z_hi, n_u, n_v, v0, v1,
+                                               out, b, w);
+  CS_COUNT_LAUNCH();
+  CS_CHECK_CUDA(cudaGetLastError());
+  return CS_OK;
+}
+
 template <int MODE>
 static int launch_interp(const float* vol, int nx, int ny, int nz, int z_lo,
                          int z_hi, const double* grid6, const double* geom,
@@ -451,49 +479,47 @@ static int launch_interp(const float* vol, int nx, int ny, int nz, int z_lo,
   if ((rc = upload_geometry(geom, n_a, s, &dgeom))) return rc;
   const int maxl = max_layers();
   // main-axis-layered kernel unless disabled (CS_FWD_MLAYER=0) or the
-  // x / y extents exceed the layer limit (then z-layers, sub-slabbed)
+  // x / y extents exceed the layer limit (then z-layers)
   static const char* ml_knob = getenv("CS_FWD_MLAYER");
-  if (!(ml_knob && ml_knob[0] == '0') && nx <= maxl && ny <= maxl &&
-      z_hi - z_lo <= max_layered_height()) {
-    rc = launch_mlayer<MODE>(vol, nx, ny, nz, z_lo, z_hi, G, geom, dgeom, n_a,
-                             n_u, n_v, step_max, out, b, w, s);
-    release_geometry(dgeom, s);
-    return rc;
-  }
-  // Slabs taller than the layer limit go through in sub-slabs;
-  // the first sub-slab applies MODE, the rest accumulate.
-  const dim3 block(128);
+  const bool ml = !(ml_knob && ml_knob[0] == '0') && nx <= maxl && ny <= maxl;
+  // The slab goes through the texture in sub-slabs of at most h planes
+  // (the first applies MODE, the rest accumulate): h starts at the
+  // texture limit and halves whenever the texture array does not fit in
+  // device memory (the array is a copy of the sub-slab: a slab planned to
+  // fill HBM would not fit twice).
+  int h = min(z_hi - z_lo, ml ? max_layered_height() : maxl);
   const size_t plane = (size_t)nx * ny;
-  for (int s0 = z_lo; s0 < z_hi; s0 += maxl) {
-    const int s1 = min(z_hi, s0 + maxl);
+  for (int s0 = z_lo; s0 < z_hi;) {
+    const int s1 = min(z_hi, s0 + h);
     const bool first = s0 == z_lo;
-    int v0 = 0, v1 = n_v;
-    if (MODE != FWD_RESIDUAL && cull_enabled())
-      slab_row_band(geom, n_a, G, s0, s1, n_v, &v0, &v1);
-    if (first && MODE == FWD_OVERWRITE &&
-        (rc = zero_rows_outside(out, n_a, n_u, n_v, v0, v1, s))) {
-      release_geometry(dgeom, s);
-      return rc;
+    const float* vs = vol + (size_t)(s0 - z_lo) * plane;
+    if (ml) {
+      rc = first ? launch_mlayer<MODE>(vs, nx, ny, nz, s0, s1, G, geom, dgeom,
+                                       n_a, n_u, n_v, step_max, out, b, w, s)
+                 : launch_mlayer<FWD_ACCUMULATE>(vs, nx, ny, nz, s0, s1, G,
+                                                 geom, dgeom, n_a, n_u, n_v,
+                                                 step_max, out, nullptr,
+                                                 nullptr, s);
+    } else {
+      rc = first ? launch_zlayer<MODE>(vs, nx, ny, nz, s0, s1, G, geom, dgeom,
+                                       n_a, n_u, n_v, step_max, out, b, w, s)
+                 : launch_zlayer<FWD_ACCUMULATE>(vs, nx, ny, nz, s0, s1, G,
+                                                 geom, dgeom, n_a, n_u, n_v,
+                                                 step_max, out, nullptr,
+                                                 nullptr, s);
     }
-    if (v1 <= v0) continue;
-    const dim3 grid((n_u + FWD_TILE_U - 1) / FWD_TILE_U,
-                    (v1 - v0 + FWD_TILE_V - 1) / FWD_TILE_V, n_a);
-    LayeredTexture* t = nullptr;
-    if ((rc = load_layered(TEX_VOLUME, vol + (size_t)(s0 - z_lo) * plane, nx,
-                           ny, s1 - s0, s, &t))) {
-      release_geometry(dgeom, s);
-      return rc;
+    // nothing was launched for a sub-slab whose array failed: retry it
+    // smaller (not the residual epilogue, which needs the whole slab)
+    if (rc == CS_ERR_CUDA && strstr(cs_last_error(), "out of memory") &&
+        MODE != FWD_RESIDUAL && h > 8) {
+      h = (h + 1) / 2;
+      continue;
     }
-    auto kern = first ? fwd_interp_kernel<MODE>
-                      : fwd_interp_kernel<FWD_ACCUMULATE>;
-    kern<<<grid, block, 0, s>>>(t->tex, dgeom, G, step_max, s0, s1, n_u, n_v,
-                                v0, v1, out, first ? b : nullptr,
-                                first ? w : nullptr);
-    CS_COUNT_LAUNCH();
-    CS_CHECK_CUDA(cudaGetLastError());
+    if (rc) break;
+    s0 = s1;
   }
   release_geometry(dgeom, s);
-  return CS_OK;
+  return rc;
 }
 
 }  // namespace cs

@@ -123,6 +123,14 @@ int acquire_layered(TexRole role, int w, int h, int layers, cudaStream_t s,
     t = LayeredTexture();
   }
   if (!t.array) {
+    // test knob: arrays above CS_TEX_MAX_MB fail as out of memory
+    static const char* cap_knob = getenv("CS_TEX_MAX_MB");
+    if (cap_knob && (double)w * h * layers * sizeof(float) >
+                        atof(cap_knob) * 1048576.0) {
+      set_error("layered texture %dx%dx%d: out of memory (CS_TEX_MAX_MB)", w,
+                h, layers);
+      return CS_ERR_CUDA;
+    }
     int rc = make_texture(t, w, h, layers);
     if (rc) return rc;
   }

@@ -608,3 +608,42 @@ def test_release_cache_then_reuse():
     K.fwd_interp(x, g, (0, 6), (0, 12), p2)
     assert torch.equal(p1, p2)
     K.release_cache()
+
+
+def test_ax_subslabs_when_texture_does_not_fit_subprocess():
+    """When the texture copy of a slab does not fit in device memory the Ax
+    halves its sub-slab height and accumulates (simulated with the
+    CS_TEX_MAX_MB knob, read once: subprocess); overwrite / accumulate Ax
+    on both texture layouts against the oracle."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path[:0] = [%r, %r]\n"
+        "import numpy as np, torch, paper_1905_03748_b200 as cs\n"
+        "from paper_1905_03748_b200 import kernels as K\n"
+        "from conftest import to_oracle, rel_l2\n"
+        "from oracle import oracle as O\n"
+        "from test_gpu_parity import _odd_geometry\n"
+        "g = _odd_geometry(40, 36, 48, 44, 40, 5)\n"
+        "og = to_oracle(g)\n"
+        "x = np.random.default_rng(8).random((48, 36, 40), dtype=np.float32)\n"
+        "xd = torch.from_numpy(x).cuda()\n"
+        "p = torch.full((5, 40, 44), 7.0, device='cuda')\n"
+        "n0 = K.launch_count()\n"
+        "K.fwd_interp(xd, g, (0, 5), (0, 48), p)\n"
+        "n1 = K.launch_count() - n0\n"
+        "import os; assert n1 >= (16 if os.environ['CS_FWD_MLAYER'] == '1' else 4), n1\n"
+        "ref = O.fwd_interp(x, og)\n"
+        "e1 = rel_l2(p.cpu(), ref)\n"
+        "K.fwd_interp(xd[10:40].contiguous(), g, (0, 5), (10, 40), p, accumulate=True)\n"
+        "e2 = rel_l2(p.cpu(), ref + O.fwd_interp(x[10:40], og, (0, 5), (10, 40)))\n"
+        "print(e1, e2, K.launch_count()); assert e1 <= 1e-5 and e2 <= 1e-5\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+         os.path.dirname(os.path.abspath(__file__)))
+    for ml in ("1", "0"):
+        # 48 planes x 40 x 36 floats = 270 KiB; cap 0.08 MiB -> 12-plane pieces
+        env = dict(os.environ, CS_TEX_MAX_MB="0.08", CS_FWD_MLAYER=ml)
+        r = subprocess.run([sys.executable, "-c", code], env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, (ml, r.stderr[-2000:])
