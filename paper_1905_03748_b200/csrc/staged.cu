@@ -67,7 +67,14 @@ __device__ __forceinline__ void st_red4(float* p, float a, float b, float c,
 // fixed_point_budget); there the 64-bit box keeps the full 2^-22-of-max-tap
 // resolution at twice the shared memory per entry.
 template <int OP, int M, int MODE, bool WIDE = false>
-__global__ void __launch_bounds__(ST_THREADS, 3)
+// 4 CTAs/SM: <= 64 registers (no spills) and 54 KB boxes (4 x 54 KB + the
+// static arrays fit the 228 KB of an SM).  r01 A/B at config 2: 3 CTAs x
+// 64 KB 359 GUPS (dense 192); 4 x 52 / 54 / 56 KB 372 / 375 / 356 (56 KB no
+// longer fits 4); 5 CTAs (48 registers, spills) 326.
+#ifndef ST_MINB
+#define ST_MINB 4
+#endif
+__global__ void __launch_bounds__(ST_THREADS, ST_MINB)
     staged_kernel(const float* __restrict__ vol_in, float* __restrict__ vol_acc,
                   const AngleGeom* __restrict__ geom,
                   const int* __restrict__ view_ids, Grid G, double step_max,
@@ -596,7 +603,7 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     CS_CHECK_CUDA(e);
   }
   static const char* kb_knob = getenv("CS_STAGED_SMEM_KB");
-  const size_t smem = (kb_knob ? (size_t)atoi(kb_knob) : 64) * 1024;
+  const size_t smem = (kb_knob ? (size_t)atoi(kb_knob) : 54) * 1024;
   const int cap = (int)(smem / sizeof(float));
   float budget =
       OP == OP_BWD ? fixed_point_budget(grid6, nx, ny, nz, geom, n_a, n_u, n_v,
