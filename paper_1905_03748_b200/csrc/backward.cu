@@ -89,11 +89,13 @@ __global__ void __launch_bounds__(128)
 // rule, _kernels.py:385-394).  The bilinear taps are then 4 shared loads
 // instead of one texture gather: the texture path is bound by its 16-byte
 // writeback per voxel-view (ncu: tex writeback 99.7%, issue 28%).
+// 7 CTAs/SM x 28 KB footprint buffers (r01 A/B at config 2: 6 x 32 KB 892
+// GUPS, 7 x 28 KB 917, 8 x 24 / 20 KB 883 / 894 -- spills at 64 registers)
 #ifndef FS_MINB
-#define FS_MINB 6
+#define FS_MINB 7
 #endif
 #ifndef CS_FS_CAP
-#define CS_FS_CAP 8192
+#define CS_FS_CAP 7168
 #endif
 constexpr int FS_TX = 16, FS_TY = 8, FS_NB = 16, FS_CAP = CS_FS_CAP;
 
