@@ -66,15 +66,12 @@ __device__ __forceinline__ void st_red4(float* p, float a, float b, float c,
 // when many rays cross a voxel (detector pixels much finer than voxels:
 // fixed_point_budget); there the 64-bit box keeps the full 2^-22-of-max-tap
 // resolution at twice the shared memory per entry.
-template <int OP, int M, int MODE, bool WIDE = false>
-// 4 CTAs/SM: <= 64 registers (no spills) and 54 KB boxes (4 x 54 KB + the
-// static arrays fit the 228 KB of an SM).  r01 A/B at config 2: 3 CTAs x
-// 64 KB 359 GUPS (dense 192); 4 x 52 / 54 / 56 KB 372 / 375 / 356 (56 KB no
-// longer fits 4); 5 CTAs (48 registers, spills) 326.
-#ifndef ST_MINB
-#define ST_MINB 4
-#endif
-__global__ void __launch_bounds__(ST_THREADS, ST_MINB)
+//
+// MINB = CTAs per SM: 3 (72 registers, 64 KB boxes) or 4 (64 registers, 54 KB
+// boxes; 4 x 54 KB + the static arrays fit an SM's 228 KB), chosen per launch
+// by the slab size (launch_staged).
+template <int OP, int M, int MODE, bool WIDE = false, int MINB = 3>
+__global__ void __launch_bounds__(ST_THREADS, MINB)
     staged_kernel(const float* __restrict__ vol_in, float* __restrict__ vol_acc,
                   const AngleGeom* __restrict__ geom,
                   const int* __restrict__ view_ids, Grid G, double step_max,
@@ -602,8 +599,14 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     release_geometry(dgeom, s);
     CS_CHECK_CUDA(e);
   }
+  // Occupancy by slab size (r01 A/B, matched, 32-360 views): 4 CTAs/SM x
+  // 54 KB boxes win up to 512^3 (+2-4%), 3 x 64 KB above (+4% at 768^3, +5%
+  // at 1024^3, +10% at 2048^3: the smaller boxes take more half-depth chunks
+  // and flushes, which cost more once the slab is far beyond L2).  5 CTAs
+  // (48 registers) spill.
+  const bool four = (double)(z_hi - z_lo) * nx * ny <= 134217728.0;  // 512^3
   static const char* kb_knob = getenv("CS_STAGED_SMEM_KB");
-  const size_t smem = (kb_knob ? (size_t)atoi(kb_knob) : 54) * 1024;
+  const size_t smem = (kb_knob ? (size_t)atoi(kb_knob) : four ? 54 : 64) * 1024;
   const int cap = (int)(smem / sizeof(float));
   float budget =
       OP == OP_BWD ? fixed_point_budget(grid6, nx, ny, nz, geom, n_a, n_u, n_v,
@@ -679,8 +682,14 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     const int rv = ST_TV / lane_stride;
     return (unsigned)((band[c][1] - band[c][0] + rv - 1) / rv);
   };
-  auto k0 = wide ? staged_kernel<OP, 0, MODE, true> : staged_kernel<OP, 0, MODE>;
-  auto k1 = wide ? staged_kernel<OP, 1, MODE, true> : staged_kernel<OP, 1, MODE>;
+  auto k0 = four ? (wide ? staged_kernel<OP, 0, MODE, true, 4>
+                         : staged_kernel<OP, 0, MODE, false, 4>)
+                  : (wide ? staged_kernel<OP, 0, MODE, true, 3>
+                          : staged_kernel<OP, 0, MODE, false, 3>);
+  auto k1 = four ? (wide ? staged_kernel<OP, 1, MODE, true, 4>
+                         : staged_kernel<OP, 1, MODE, false, 4>)
+                  : (wide ? staged_kernel<OP, 1, MODE, true, 3>
+                          : staged_kernel<OP, 1, MODE, false, 3>);
   // the dynamic shared-memory opt-in is per device: set it once on each
   // (the executor drives several GPUs from one process)
   static std::atomic<unsigned long long> attr_done{0};
@@ -688,9 +697,14 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   cudaGetDevice(&dev_ord);
   const unsigned long long bit = 1ull << (dev_ord & 63);
   if (!(attr_done.load() & bit)) {
-    for (auto k : {staged_kernel<OP, 0, MODE>, staged_kernel<OP, 1, MODE>,
-                   staged_kernel<OP, 0, MODE, true>,
-                   staged_kernel<OP, 1, MODE, true>})
+    for (auto k : {staged_kernel<OP, 0, MODE, false, 3>,
+                   staged_kernel<OP, 1, MODE, false, 3>,
+                   staged_kernel<OP, 0, MODE, true, 3>,
+                   staged_kernel<OP, 1, MODE, true, 3>,
+                   staged_kernel<OP, 0, MODE, false, 4>,
+                   staged_kernel<OP, 1, MODE, false, 4>,
+                   staged_kernel<OP, 0, MODE, true, 4>,
+                   staged_kernel<OP, 1, MODE, true, 4>})
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            200 * 1024);
     attr_done.fetch_or(bit);

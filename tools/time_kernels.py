@@ -28,20 +28,19 @@ ops = {
     "matched_dense": lambda: K.bwd_matched(dense, g, (0, A), (0, n), acc),
     "siddon": lambda: K.fwd_siddon(vol, g, (0, A), (0, n), y),
 }
-u2 = torch.empty_like(vol)
-ss = torch.zeros(1, dtype=torch.float64, device=dev)
-p3 = torch.zeros((3, n, n, n), device=dev)
-q3 = torch.empty_like(p3)
-
-
-def tv_gd():
-    K.tv_grad_sumsq(vol, (0, n), ss)
-    K.tv_step(vol, u2, 1e-3, ss, 1.0)
-
-
-ops["tv_gd_iter"] = tv_gd
-ops["rof_iter"] = lambda: K.rof_iter(vol, p3, q3, 0.1)
 only = os.environ.get("PROF_ONLY")
+if not only or "tv_gd_iter" in only or "rof_iter" in only:
+    u2 = torch.empty_like(vol)
+    ss = torch.zeros(1, dtype=torch.float64, device=dev)
+    p3 = torch.zeros((3, n, n, n), device=dev)
+    q3 = torch.empty_like(p3)
+
+    def tv_gd():
+        K.tv_grad_sumsq(vol, (0, n), ss)
+        K.tv_step(vol, u2, 1e-3, ss, 1.0)
+
+    ops["tv_gd_iter"] = tv_gd
+    ops["rof_iter"] = lambda: K.rof_iter(vol, p3, q3, 0.1)
 if only:
     ops = {k: v for k, v in ops.items() if k in only.split(",")}
 out = {}
