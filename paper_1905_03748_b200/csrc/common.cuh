@@ -203,20 +203,20 @@ __device__ __forceinline__ float int_to_float(int i) {
   return __int_as_float(i + 0x4B400000) - 12582912.f;
 }
 
-// Sample range [k0, k1) whose trilinear z-support can touch global slices
-// [z_lo, z_hi): qz(k) in [z_lo - 1, z_hi).  Conservative by two samples;
-// exact slab membership is decided per tap in the march loop with the same
-// fp32 qz a monolithic launch computes, so slab partial sums add up to the
-// monolithic result.
-__device__ __forceinline__ void slab_k_range(const Ray& r, const March& m,
-                                             const Grid& G, int z_lo,
-                                             int z_hi, long long& k0,
+// Sample range [k0, k1) whose trilinear support along `axis` can touch
+// planes [lo, hi): q(axis, k) in [lo - 1, hi) (slab_k_range: z, the slab).
+// Conservative by two samples; exact membership is decided per tap in the
+// march loop from the same exact positions a monolithic launch computes, so
+// slab partial sums add up to the monolithic result.
+__device__ __forceinline__ void axis_k_range(const Ray& r, const March& m,
+                                             int axis, int n_axis, int lo_i,
+                                             int hi_i, long long& k0,
                                              long long& k1) {
   k0 = 0;
   k1 = r.n;
-  if (z_lo <= 0 && z_hi >= G.n[2]) return;
-  double B = m.Bd[2], A = m.Ad[2];
-  double lo = (double)z_lo - 1.0, hi = (double)z_hi;
+  if (lo_i <= 0 && hi_i >= n_axis) return;
+  double B = m.Bd[axis], A = m.Ad[axis];
+  double lo = (double)lo_i - 1.0, hi = (double)hi_i;
   if (fabs(B) < 1e-30) {
     if (A < lo - 1.0 || A > hi + 1.0) k1 = 0;
     return;
@@ -230,6 +230,13 @@ __device__ __forceinline__ void slab_k_range(const Ray& r, const March& m,
   double fa = floor(ka) - 2.0, fb = ceil(kb) + 3.0;
   if (fa > 0.0) k0 = fa > (double)r.n ? r.n : (long long)fa;
   if (fb < (double)r.n) k1 = fb < 0.0 ? 0 : (long long)fb;
+}
+
+__device__ __forceinline__ void slab_k_range(const Ray& r, const March& m,
+                                             const Grid& G, int z_lo,
+                                             int z_hi, long long& k0,
+                                             long long& k1) {
+  axis_k_range(r, m, 2, G.n[2], z_lo, z_hi, k0, k1);
 }
 
 // tld4 (gather) on a 2D layered float texture: returns the 2x2 footprint a

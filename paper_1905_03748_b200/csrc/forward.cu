@@ -124,9 +124,9 @@ __global__ void __launch_bounds__(128, FWD_ML_MINB)
     fwd_mlayer_kernel(cudaTextureObject_t tex,
                       const AngleGeom* __restrict__ geom,
                       const int* __restrict__ view_ids, Grid G,
-                      double step_max, int z_lo, int z_hi, int n_u, int n_v,
-                      int v_base, int v_end, float* __restrict__ out,
-                      const float* __restrict__ b,
+                      double step_max, int z_lo, int z_hi, int m_lo,
+                      int m_hi, int n_u, int n_v, int v_base, int v_end,
+                      float* __restrict__ out, const float* __restrict__ b,
                       const float* __restrict__ w) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int u = blockIdx.x * FWD_TILE_U + (warp & 1) * 8 + (lane >> 2);
@@ -139,12 +139,16 @@ __global__ void __launch_bounds__(128, FWD_ML_MINB)
   if (r.n > 0) {
     March m;
     march_params(r, G, m);
-    long long k0l, k1l;
+    long long k0l, k1l, k0m, k1m;
     slab_k_range(r, m, G, z_lo, z_hi, k0l, k1l);
-    const int k0 = (int)k0l, k1 = (int)k1l;
+    // the texture holds M planes [m_lo, m_hi) (all of them unless n_M
+    // exceeds the layer limit); layer = plane - m_lo
     constexpr int T = 1 - M;
-    const int top = G.n[M] - 1;
-    long long qm = q_at(m, k0, M), qt = q_at(m, k0, T), qz = q_at(m, k0, 2);
+    axis_k_range(r, m, M, G.n[M], m_lo, m_hi, k0m, k1m);
+    const int k0 = (int)max(k0l, k0m), k1 = (int)min(k1l, k1m);
+    const int top = m_hi - m_lo - 1;
+    long long qm = q_at(m, k0, M) - ((long long)m_lo << QF), qt = q_at(m, k0, T),
+              qz = q_at(m, k0, 2);
     const long long bm = m.Bq[M], bt = m.Bq[T], bz = m.Bq[2];
     // Software-pipelined: the gathers of sample k + 1 are issued before
     // sample k is interpolated -- with the quads skipping together the
@@ -228,16 +232,16 @@ __global__ void __launch_bounds__(128, FWD_ML_MINB)
 __global__ void __launch_bounds__(256)
     fill_xlayers_kernel(cudaSurfaceObject_t surf,
                         const float* __restrict__ vol, int nx, int ny, int nzs,
-                        int zr) {
+                        int zr, int l0, int l1) {
   __shared__ float brick[8][32][33];
-  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32, z0 = blockIdx.z * 8;
+  const int x0 = l0 + blockIdx.x * 32, y0 = blockIdx.y * 32, z0 = blockIdx.z * 8;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
   const size_t plane = (size_t)nx * ny;
   for (int zz = 0; zz < 8; zz++) {
     const int z = z0 + zz;
     for (int j = ty; j < 32; j += 8) {
       const int x = x0 + tx, y = y0 + j;
-      brick[zz][j][tx] = (x < nx && y < ny && z < nzs)
+      brick[zz][j][tx] = (x < l1 && y < ny && z < nzs)
                              ? vol[(size_t)z * plane + (size_t)y * nx + x]
                              : 0.f;
     }
@@ -245,9 +249,9 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const int z = z0 + ty, y = y0 + tx;
   if (z >= zr || y >= ny) return;
-  for (int j = 0; j < 32 && x0 + j < nx; j++)
+  for (int j = 0; j < 32 && x0 + j < l1; j++)
     surf2DLayeredwrite(brick[ty][tx][j], surf, y * (int)sizeof(float), z,
-                       x0 + j);
+                       x0 + j - l0);
 }
 
 // Slab [nzs, ny, nx] -> y-layers (layer y, texel (x, z)): a CTA writes a
@@ -255,34 +259,37 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     fill_ylayers_kernel(cudaSurfaceObject_t surf,
                         const float* __restrict__ vol, int nx, int ny, int nzs,
-                        int zr) {
+                        int zr, int l0) {
   const int x = blockIdx.x * 32 + threadIdx.x;
-  const int z = blockIdx.y * 8 + threadIdx.y, y = blockIdx.z;
+  const int z = blockIdx.y * 8 + threadIdx.y, y = l0 + blockIdx.z;
   if (x >= nx || z >= zr) return;
   surf2DLayeredwrite(z < nzs ? vol[((size_t)z * ny + y) * nx + x] : 0.f, surf,
-                     x * (int)sizeof(float), z, y);
+                     x * (int)sizeof(float), z, y - l0);
 }
 
-// Loads slab planes [0, nzs) of `vol` as main-axis-M layers.
+// Loads slab planes [0, nzs) of `vol`, M planes [l0, l1), as main-axis-M
+// layers (layer = plane - l0).
 static int load_mlayers(int M, const float* vol, int nx, int ny, int nzs,
-                        cudaStream_t s, LayeredTexture** t) {
+                        int l0, int l1, cudaStream_t s, LayeredTexture** t) {
   const TexRole role = (M == 1 && nx != ny) ? TEX_VOL_M2 : TEX_VOL_M;
   // slabs of different heights reuse a taller array (no reallocation and
   // stream drain per slab)
-  int rc = M == 0 ? acquire_layered(role, ny, nzs, nx, s, t, true)
-                  : acquire_layered(role, nx, nzs, ny, s, t, true);
+  int rc = M == 0 ? acquire_layered(role, ny, nzs, l1 - l0, s, t, true)
+                  : acquire_layered(role, nx, nzs, l1 - l0, s, t, true);
   if (rc) return rc;
   // rows past the slab must read zero: slab_k_range keeps <= 3 samples
   // beyond the slab (<= 1.5 planes at |dz| <= 1/2 voxel per sample), so a
   // taller array gets 4 zero guard rows
   const int zr = min((*t)->h, nzs + 4);
   if (M == 0) {
-    fill_xlayers_kernel<<<dim3((nx + 31) / 32, (ny + 31) / 32, (zr + 7) / 8),
+    fill_xlayers_kernel<<<dim3((l1 - l0 + 31) / 32, (ny + 31) / 32,
+                               (zr + 7) / 8),
                           dim3(32, 8), 0, s>>>((*t)->surf, vol, nx, ny, nzs,
-                                               zr);
+                                               zr, l0, l1);
   } else {
-    fill_ylayers_kernel<<<dim3((nx + 31) / 32, (zr + 7) / 8, ny), dim3(32, 8),
-                          0, s>>>((*t)->surf, vol, nx, ny, nzs, zr);
+    fill_ylayers_kernel<<<dim3((nx + 31) / 32, (zr + 7) / 8, l1 - l0),
+                          dim3(32, 8), 0, s>>>((*t)->surf, vol, nx, ny, nzs,
+                                               zr, l0);
   }
   CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
@@ -322,18 +329,34 @@ static int launch_mlayer(const float* vol, int nx, int ny, int nz, int z_lo,
     slab_row_band(geom, n_a, G, z_lo, z_hi, n_v, &v0, &v1);
   if (MODE == FWD_OVERWRITE)
     rc = zero_rows_outside(out, n_a, n_u, n_v, v0, v1, s);
+  // n_M over the layer limit: the M planes go through in pieces of <= maxl
+  // layers, the first applying MODE (not the residual: the caller keeps
+  // that to one piece), the rest accumulating
+  const int maxl = max_layers();
   for (int c = 0; c < 2 && rc == CS_OK && v1 > v0; c++) {
     if (!cnt[c]) continue;
-    LayeredTexture* t = nullptr;
-    if ((rc = load_mlayers(c, vol, nx, ny, z_hi - z_lo, s, &t))) break;
-    const dim3 grid((n_u + FWD_TILE_U - 1) / FWD_TILE_U,
-                    (v1 - v0 + FWD_TILE_V - 1) / FWD_TILE_V, cnt[c]);
-    auto kern = c == 0 ? fwd_mlayer_kernel<MODE, 0> : fwd_mlayer_kernel<MODE, 1>;
-    kern<<<grid, 128, 0, s>>>(t->tex, dgeom, ids + (c ? cnt[0] : 0), G,
-                              step_max, z_lo, z_hi, n_u, n_v, v0, v1, out, b,
-                              w);
-    CS_COUNT_LAUNCH();
-    if ((e = cudaGetLastError()) != cudaSuccess) break;
+    const int n_m = c == 0 ? nx : ny;
+    const int np = (n_m + maxl - 1) / maxl;
+    for (int p = 0; p < np && rc == CS_OK; p++) {
+      const int l0 = (int)((long long)n_m * p / np);
+      const int l1 = (int)((long long)n_m * (p + 1) / np);
+      LayeredTexture* t = nullptr;
+      if ((rc = load_mlayers(c, vol, nx, ny, z_hi - z_lo, l0, l1, s, &t)))
+        break;
+      const dim3 grid((n_u + FWD_TILE_U - 1) / FWD_TILE_U,
+                      (v1 - v0 + FWD_TILE_V - 1) / FWD_TILE_V, cnt[c]);
+      auto kern = p == 0 ? (c == 0 ? fwd_mlayer_kernel<MODE, 0>
+                                   : fwd_mlayer_kernel<MODE, 1>)
+                         : (c == 0 ? fwd_mlayer_kernel<FWD_ACCUMULATE, 0>
+                                   : fwd_mlayer_kernel<FWD_ACCUMULATE, 1>);
+      kern<<<grid, 128, 0, s>>>(t->tex, dgeom, ids + (c ? cnt[0] : 0), G,
+                                step_max, z_lo, z_hi, l0, l1, n_u, n_v, v0, v1,
+                                out, p == 0 ? b : nullptr,
+                                p == 0 ? w : nullptr);
+      CS_COUNT_LAUNCH();
+      if ((e = cudaGetLastError()) != cudaSuccess) break;
+    }
+    if (e != cudaSuccess) break;
   }
   cudaFreeAsync(ids, s);
   CS_CHECK_CUDA(e);
@@ -478,10 +501,12 @@ static int launch_interp(const float* vol, int nx, int ny, int nz, int z_lo,
   AngleGeom* dgeom = nullptr;
   if ((rc = upload_geometry(geom, n_a, s, &dgeom))) return rc;
   const int maxl = max_layers();
-  // main-axis-layered kernel unless disabled (CS_FWD_MLAYER=0) or the
-  // x / y extents exceed the layer limit (then z-layers)
+  // main-axis-layered kernel unless disabled (CS_FWD_MLAYER=0)
   static const char* ml_knob = getenv("CS_FWD_MLAYER");
-  const bool ml = !(ml_knob && ml_knob[0] == '0') && nx <= maxl && ny <= maxl;
+  // (x / y extents over the layer limit go through in layer pieces, which
+  // the residual epilogue cannot: it keeps the z-layers there)
+  const bool ml = !(ml_knob && ml_knob[0] == '0') &&
+                  ((nx <= maxl && ny <= maxl) || MODE != FWD_RESIDUAL);
   // The slab goes through the texture in sub-slabs of at most h planes
   // (the first applies MODE, the rest accumulate): h starts at the
   // texture limit and halves whenever the texture array does not fit in

@@ -59,6 +59,9 @@ int max_layers() {
     if (cudaDeviceGetAttribute(&dims[0], cudaDevAttrMaxTexture2DLayeredLayers,
                                dev) != cudaSuccess)
       dims[0] = 2048;
+    // test knob: a lower limit exercises the layer pieces / sub-slabs
+    const char* k = getenv("CS_MAX_LAYERS");
+    if (k && atoi(k) > 0 && atoi(k) < dims[0]) dims[0] = atoi(k);
     v = dims[0];
   }
   return v;

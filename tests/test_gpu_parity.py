@@ -647,3 +647,42 @@ def test_ax_subslabs_when_texture_does_not_fit_subprocess():
         r = subprocess.run([sys.executable, "-c", code], env=env,
                            capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, (ml, r.stderr[-2000:])
+
+
+def test_ax_layer_pieces_subprocess():
+    """x / y extents over the layered-texture limit (forced low with the
+    CS_MAX_LAYERS knob, read once: subprocess): the main-axis Ax goes through
+    in layer pieces (k ranges clipped per piece, first piece overwrites,
+    the rest accumulate), the z-layered Ax in sub-slabs; both against the
+    oracle, full volume, a slab and an accumulate launch."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path[:0] = [%r, %r]\n"
+        "import numpy as np, torch, paper_1905_03748_b200 as cs\n"
+        "from paper_1905_03748_b200 import kernels as K\n"
+        "from conftest import to_oracle, rel_l2\n"
+        "from oracle import oracle as O\n"
+        "from test_gpu_parity import _odd_geometry\n"
+        "g = _odd_geometry(40, 36, 30, 44, 40, 7)\n"
+        "og = to_oracle(g)\n"
+        "x = np.random.default_rng(12).random((30, 36, 40), dtype=np.float32)\n"
+        "xd = torch.from_numpy(x).cuda()\n"
+        "p = torch.full((7, 40, 44), 3.0, device='cuda')\n"
+        "n0 = K.launch_count()\n"
+        "K.fwd_interp(xd, g, (0, 7), (0, 30), p)\n"
+        "n1 = K.launch_count() - n0\n"
+        "ref = O.fwd_interp(x, og)\n"
+        "e1 = rel_l2(p.cpu(), ref)\n"
+        "K.fwd_interp(xd[5:22].contiguous(), g, (0, 7), (5, 22), p, accumulate=True)\n"
+        "e2 = rel_l2(p.cpu(), ref + O.fwd_interp(x[5:22], og, (0, 7), (5, 22)))\n"
+        "print(e1, e2, n1); assert e1 <= 1e-5 and e2 <= 1e-5\n"
+        "import os; assert n1 >= (12 if os.environ['CS_FWD_MLAYER'] == '1' else 2), n1\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+         os.path.dirname(os.path.abspath(__file__)))
+    for ml in ("1", "0"):
+        env = dict(os.environ, CS_MAX_LAYERS="16", CS_FWD_MLAYER=ml)
+        r = subprocess.run([sys.executable, "-c", code], env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, (ml, r.stderr[-2000:])
