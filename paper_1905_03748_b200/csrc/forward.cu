@@ -116,6 +116,14 @@ __global__ void __launch_bounds__(128, FWD_MINB)
 // is the previous far layer); a T or z change re-gathers both.  T and z
 // outside the texture read the border zero (the reference's padding and
 // the slab's z range); layers are masked in the weights.
+#ifndef ML_WU
+#define ML_WU 2
+#endif
+#ifndef ML_WARP_U
+#define ML_WARP_U 8
+#endif
+constexpr int ML_TILE_U = ML_WARP_U * ML_WU,
+              ML_TILE_V = (32 / ML_WARP_U) * (4 / ML_WU);
 #ifndef FWD_ML_MINB
 #define FWD_ML_MINB 8  // 64 registers (two prefetch buffers), 32 warps/SM
 #endif
@@ -129,8 +137,12 @@ __global__ void __launch_bounds__(128, FWD_ML_MINB)
                       float* __restrict__ out, const float* __restrict__ b,
                       const float* __restrict__ w) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int u = blockIdx.x * FWD_TILE_U + (warp & 1) * 8 + (lane >> 2);
-  const int v = v_base + blockIdx.y * FWD_TILE_V + (warp >> 1) * 4 + (lane & 3);
+  // warp = ML_WARP_U u x (32 / ML_WARP_U) v rays, v fastest (quads = 4
+  // v-adjacent lanes); the CTA's 4 warps tile ML_WU x (4 / ML_WU) along (u, v)
+  constexpr int WV = 32 / ML_WARP_U;
+  const int u = blockIdx.x * ML_TILE_U + (warp % ML_WU) * ML_WARP_U + lane / WV;
+  const int v = v_base + blockIdx.y * ML_TILE_V + (warp / ML_WU) * WV +
+                lane % WV;
   const int a = view_ids[blockIdx.z];
   if (u >= n_u || v >= v_end) return;
   Ray r;
@@ -343,8 +355,8 @@ static int launch_mlayer(const float* vol, int nx, int ny, int nz, int z_lo,
       LayeredTexture* t = nullptr;
       if ((rc = load_mlayers(c, vol, nx, ny, z_hi - z_lo, l0, l1, s, &t)))
         break;
-      const dim3 grid((n_u + FWD_TILE_U - 1) / FWD_TILE_U,
-                      (v1 - v0 + FWD_TILE_V - 1) / FWD_TILE_V, cnt[c]);
+      const dim3 grid((n_u + ML_TILE_U - 1) / ML_TILE_U,
+                      (v1 - v0 + ML_TILE_V - 1) / ML_TILE_V, cnt[c]);
       auto kern = p == 0 ? (c == 0 ? fwd_mlayer_kernel<MODE, 0>
                                    : fwd_mlayer_kernel<MODE, 1>)
                          : (c == 0 ? fwd_mlayer_kernel<FWD_ACCUMULATE, 0>
