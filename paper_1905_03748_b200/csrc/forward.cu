@@ -112,10 +112,10 @@ __global__ void __launch_bounds__(128, FWD_MINB)
 // v-ADJACENT rays: rays of one detector column share their xy path and,
 // with equal sample counts, their x / y sample positions, so their cells
 // change together -- the texture pipe charges a tld4 per quad with any
-// active lane.  An M-advance by one plane re-gathers one layer (the other
-// is the previous far layer); a T or z change re-gathers both.  T and z
+// active lane.  A cell change re-gathers both layers (iM, iM + 1).  T and z
 // outside the texture read the border zero (the reference's padding and
-// the slab's z range); layers are masked in the weights.
+// the slab's z range); layers outside [0, n_M) -- or outside the piece of
+// layers this launch holds -- are masked in the weights.
 #ifndef ML_WU
 #define ML_WU 2
 #endif
@@ -162,18 +162,16 @@ __global__ void __launch_bounds__(128, FWD_ML_MINB)
     long long qm = q_at(m, k0, M) - ((long long)m_lo << QF), qt = q_at(m, k0, T),
               qz = q_at(m, k0, 2);
     const long long bm = m.Bq[M], bt = m.Bq[T], bz = m.Bq[2];
-    // Software-pipelined: the gathers of sample k + 1 are issued before
-    // sample k is interpolated -- with the quads skipping together the
-    // texture pipe is no longer saturated and the kernel is tld4-latency
-    // bound.  r01 A/B at config 2 (90-view launches incl. texture fills):
-    // re-gather on change 283 GUPS; one-layer M-step reuse through
-    // predicated gathers 242 (+38% instructions); one prefetch buffer 309
-    // (56 regs) / 325 (48 regs, 40 warps/SM) -- its rotation waited on the
-    // gathers just issued; two buffers (below) 344 (64 regs) / 326 (56) /
+    // Software-pipelined over two prefetch buffers: sample k+1's gathers
+    // (predicated on its cell change) go to one while sample k's data is
+    // taken from the other, gathered one iteration earlier, so the wait for
+    // a gather spans a whole iteration.  With the quads skipping together
+    // the plain loop was tld4-latency bound.  r01 A/B at config 2 (90-view
+    // launches incl. texture fills): re-gather on change 283 GUPS; one-layer
+    // M-step reuse through predicated gathers 242 (+38% instructions); one
+    // prefetch buffer 309 (56 regs) / 325 (48 regs) -- its rotation waited
+    // on the gathers just issued; two buffers 344 (64 regs) / 326 (56) /
     // 283 (48, spills).
-    // Two prefetch buffers: sample k+1's gathers go to one while sample
-    // k's data is taken from the other (gathered one iteration earlier), so
-    // the wait for a gather spans a whole iteration.
     int cm = q_cell(qm), ct = q_cell(qt), cz = q_cell(qz);
     const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
     float4 s0 = zero4, s1 = zero4, pa0 = zero4, pa1 = zero4, pb0 = zero4,
