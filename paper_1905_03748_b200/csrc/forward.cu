@@ -7,10 +7,13 @@
 // set-up is fp64 and bit-identical to the reference (_kernels.py:194-246);
 // positions are exact Q32.32 fixed point (common.cuh).  Each trilinear sample is
 // TWO texture gathers (tld4 on a 2D-layered float texture: 2x2 texels of
-// slice iz and of slice iz+1) with fp32 software weights, i.e. exact
+// two adjacent layers) with fp32 software weights, i.e. exact
 // interpolation weights (hardware filtering's 8-bit weights are 100x off
 // the parity budget) at a quarter of the point-sample
-// fetch count.  Border addressing gives the reference's zero padding in
+// fetch count.  Production: fwd_mlayer_kernel (layers = planes along the
+// view's main axis, v-adjacent texture quads, pipelined gathers);
+// fwd_interp_kernel (layers = z slices) is the A/B baseline and serves
+// the residual epilogue when x or y exceeds the layer limit.  Border addressing gives the reference's zero padding in
 // x/y; z taps are masked to the slab [z_lo, z_hi) exactly as
 // _kernels.py:259-262, and the sample range is clipped to the slab so a
 // slab launch costs only its share of the ray.
