@@ -125,6 +125,11 @@ int cs_ray_table(int nx, int ny, int nz, const double* grid6,
  * (regularization.py:127-130, :245-251 / :147). */
 int cs_tv_grad_sumsq(const float* u, int nx, int ny, int nzw, int core_lo,
                      int core_hi, double* out_sum, cs_stream_t stream);
+/* ||g||_2 over the core (regularization.py:147: np.linalg.norm(g)); the same
+ * pass as cs_tv_grad_sumsq plus a device sqrt.  Multi-GPU callers reduce the
+ * sum of squares across ranks first, so they use cs_tv_grad_sumsq. */
+int cs_tv_grad_norm(const float* u, int nx, int ny, int nzw, int core_lo,
+                    int core_hi, double* out_norm, cs_stream_t stream);
 
 /* u_out = u - step * g / norm with norm = *norm_dev (device fp64 scalar);
  * skipped (u_out = u) when norm < 1e-30 (regularization.py:150, :258-260).

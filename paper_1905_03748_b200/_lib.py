@@ -47,6 +47,7 @@ SYMBOLS: dict[str, list] = {
     "cs_bwd_fdk": [P, I, I, I, I, P, P, I, D, D, D, D, D, D, I, I, P, P],
     "cs_ray_table": [I, I, I, P, P, I, I, I, D, P, P, P, P],
     "cs_tv_grad_sumsq": [P, I, I, I, I, I, P, P],
+    "cs_tv_grad_norm": [P, I, I, I, I, I, P, P],
     "cs_tv_step": [P, P, I, I, I, D, P, D, P],
     "cs_rof_iter": [P, P, P, I, I, I, D, P],
     "cs_rof_finish": [P, P, P, I, I, I, D, P],

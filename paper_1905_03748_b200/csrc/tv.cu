@@ -337,6 +337,8 @@ int reduce_into(const double* partial, size_t n, double* out,
   return CS_OK;
 }
 
+__global__ void sqrt_in_place_kernel(double* v) { *v = sqrt(*v); }
+
 static int check_win(int nx, int ny, int nzw) {
   CS_REQUIRE(nx >= 2 && ny >= 2 && nzw >= 2, CS_ERR_ARG,
              "TV needs at least 2 voxels per axis (got %d x %d x %d)", nx, ny,
@@ -371,6 +373,17 @@ int cs_tv_grad_sumsq(const float* u, int nx, int ny, int nzw, int core_lo,
   rc = reduce_into(part, nb, out_sum, s);
   cudaFreeAsync(part, s);
   return rc;
+}
+
+int cs_tv_grad_norm(const float* u, int nx, int ny, int nzw, int core_lo,
+                    int core_hi, double* out_norm, cs_stream_t stream) {
+  int rc = cs_tv_grad_sumsq(u, nx, ny, nzw, core_lo, core_hi, out_norm,
+                            stream);
+  if (rc) return rc;
+  sqrt_in_place_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(out_norm);
+  CS_COUNT_LAUNCH();
+  CS_CHECK_CUDA(cudaGetLastError());
+  return CS_OK;
 }
 
 int cs_tv_step(const float* u, float* u_out, int nx, int ny, int nzw,

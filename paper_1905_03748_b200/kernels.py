@@ -200,6 +200,14 @@ def tv_grad_sumsq(u: torch.Tensor, core, out: torch.Tensor, stream=None):
     return out
 
 
+def tv_grad_norm(u: torch.Tensor, core, out: torch.Tensor, stream=None):
+    """out[0] = ||g||_2 over the core planes (regularization.py:147)."""
+    nz, ny, nx = u.shape
+    check(lib().cs_tv_grad_norm(dptr(_f32(u, "u")), nx, ny, nz, core[0],
+                                core[1], dptr(out), stream_ptr(stream)))
+    return out
+
+
 def tv_step(u: torch.Tensor, u_out: torch.Tensor, step: float,
             sumsq: torch.Tensor, scale: float = 1.0, stream=None):
     nz, ny, nx = u.shape

@@ -709,3 +709,21 @@ def test_ax_residual_epilogue_vs_oracle(dims):
     assert rel_l2(out.cpu(), b - ax) <= TOL_OP
     K.fwd_interp_residual(xd, g, (0, 9), bd, wd, out)
     assert rel_l2(out.cpu(), w * (b - ax)) <= TOL_OP
+
+
+def test_tv_grad_norm_and_sumsq_vs_oracle(golden):
+    """cs_tv_grad_norm / cs_tv_grad_sumsq: ||g||_2 and its square for the
+    TV subgradient g (regularization.py:127-130, :147), over the whole
+    window and over a core band, against the oracle (fp64 numpy)."""
+    import torch
+    from paper_1905_03748_b200 import kernels as K
+    f = np.asarray(golden["tv/f"], np.float32)
+    g = O.tv_subgradient(f.astype(np.float64))
+    ud = torch.from_numpy(f).cuda()
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    K.tv_grad_norm(ud, (0, f.shape[0]), out)
+    ref = float(np.linalg.norm(g))
+    assert abs(float(out) - ref) <= 1e-5 * ref
+    K.tv_grad_sumsq(ud, (5, 17), out)
+    ref2 = float((g[5:17] ** 2).sum())
+    assert abs(float(out) - ref2) <= 2e-5 * ref2
