@@ -67,7 +67,7 @@ __device__ __forceinline__ void st_red4(float* p, float a, float b, float c,
 // fixed_point_budget); there the 64-bit box keeps the full 2^-22-of-max-tap
 // resolution at twice the shared memory per entry.
 //
-// MINB = CTAs per SM: 3 (72 registers, 64 KB boxes) or 4 (64 registers, 54 KB
+// MINB = CTAs per SM: 3 (72 registers, 72 KB boxes) or 4 (64 registers, 54 KB
 // boxes; 4 x 54 KB + the static arrays fit an SM's 228 KB), chosen per launch
 // by the slab size (launch_staged).
 template <int OP, int M, int MODE, bool WIDE = false, int MINB = 3>
@@ -606,7 +606,9 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   // (48 registers) spill.
   const bool four = (double)(z_hi - z_lo) * nx * ny <= 134217728.0;  // 512^3
   static const char* kb_knob = getenv("CS_STAGED_SMEM_KB");
-  const size_t smem = (kb_knob ? (size_t)atoi(kb_knob) : four ? 54 : 64) * 1024;
+  // (3 CTAs: 72 KB boxes, +1-3% over 64 KB at 1024^3 / 2048^3; 80 KB no
+  // longer fits three)
+  const size_t smem = (kb_knob ? (size_t)atoi(kb_knob) : four ? 54 : 72) * 1024;
   const int cap = (int)(smem / sizeof(float));
   float budget =
       OP == OP_BWD ? fixed_point_budget(grid6, nx, ny, nz, geom, n_a, n_u, n_v,
