@@ -378,7 +378,7 @@ static int launch_mlayer(const float* vol, int nx, int ny, int nz, int z_lo,
 
 // Siddon traversal, _kernels.py:71-151 (fp64, midpoint attribution).
 #ifndef SID_MINB
-#define SID_MINB 10  // <= 48 registers: 40 warps/SM hide the fp64 chain latency
+#define SID_MINB 12  // 40 registers: 48 warps/SM hide the serial fp64 event chain
 #endif
 __global__ void __launch_bounds__(128, SID_MINB)
     fwd_siddon_kernel(const float* __restrict__ vol,
@@ -425,25 +425,38 @@ __global__ void __launch_bounds__(128, SID_MINB)
     // the same voxel as the division -- three fp64 divisions per piece were
     // the kernel's largest cost.
     const double ivx = 1.0 / vx, ivy = 1.0 / vy, ivz = 1.0 / vz;
+    // The voxel is taken from the midpoint once (first piece longer than
+    // 1e-12) and then stepped with the crossings: every later piece lies
+    // between the same fp64 events the reference uses, so its midpoint
+    // voxel is the stepped one (pieces <= 1e-12 are skipped by both).
+    // Bit-identical to the per-piece midpoint floor at config 2 and on
+    // every parity case; 345 -> 354 GUPS, 362 at 40 registers (r01).
+    const int sx = d[0] > 0.0 ? 1 : -1, sy = d[1] > 0.0 ? 1 : -1,
+              sz = d[2] > 0.0 ? 1 : -1;
+    int ix = 0, iy = 0, iz = 0;
+    bool have = false;
     double t = t0;
     while (t < t1 - 1e-12) {
       double tnext = fmin(fmin(tn[0], tn[1]), tn[2]);
       if (tnext > t1) tnext = t1;
       const double seg = tnext - t;
       if (seg > 1e-12) {
-        const double tm = 0.5 * (t + tnext);
-        const int ix = (int)floor((o[0] + tm * d[0] - gx0) * ivx);
-        const int iy = (int)floor((o[1] + tm * d[1] - gy0) * ivy);
-        const int iz = (int)floor((o[2] + tm * d[2] - gz0) * ivz);
-        if (ix >= 0 && ix < nx && iy >= 0 && iy < ny && iz >= z_lo &&
-            iz < z_hi)
+        if (!have) {
+          const double tm = 0.5 * (t + tnext);
+          ix = (int)floor((o[0] + tm * d[0] - gx0) * ivx);
+          iy = (int)floor((o[1] + tm * d[1] - gy0) * ivy);
+          iz = (int)floor((o[2] + tm * d[2] - gz0) * ivz);
+          have = true;
+        }
+        if ((unsigned)ix < (unsigned)nx && (unsigned)iy < (unsigned)ny &&
+            iz >= z_lo && iz < z_hi)
           acc += seg * (double)__ldg(vol + (size_t)(iz - z_lo) * plane +
                                      (size_t)iy * nx + ix);
       }
       if (tnext >= t1) break;
-#pragma unroll
-      for (int i = 0; i < 3; i++)
-        if (tn[i] <= tnext) tn[i] += dt[i];
+      if (tn[0] <= tnext) { tn[0] += dt[0]; ix += have ? sx : 0; }
+      if (tn[1] <= tnext) { tn[1] += dt[1]; iy += have ? sy : 0; }
+      if (tn[2] <= tnext) { tn[2] += dt[2]; iz += have ? sz : 0; }
       t = tnext;
     }
   }
