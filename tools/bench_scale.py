@@ -21,6 +21,7 @@
     python tools/bench_scale.py c3 [N=8] [views=1024]
     python tools/bench_scale.py c5 [n=4096] [views=32] [slab=256]
     python tools/bench_scale.py ooc [n=2048] [views=64] [budget_gib=12]
+    python tools/bench_scale.py c4 [n=1024] [views=1024] [iters=2] [block=32]
 
 Prints one JSON line per measurement.
 """
@@ -233,6 +234,48 @@ def c5(n=4096, A=32, slab=256):
         "adjoint_rel_diff": abs(lhs - rhs) / abs(lhs)}), flush=True)
 
 
+def c4(n=1024, A=1024, iters=2, block=32):
+    """Config 4 loops on one GPU, in-core: SART-TV (OS-SART block `block`
+    + TvParams(GD, inner 20, step 1e-3, ExactGlobal)) and CGLS on the
+    Shepp-Logan sinogram of a 1024^3 volume x 1024 views of a 1024^2
+    detector, device-resident inputs; seconds per
+    iteration (after a setup+1-iteration run) and the residuals."""
+    dev = torch.device("cuda", 0)
+    g = bench.make_geometry(n, A, cs)
+    x_true = cs.phantom(cs.PhantomKind.SHEPP_LOGAN_3D, g.voxel_grid,
+                        device=dev).data
+    b = cs.forward_project_slab(cs.Volume(g.voxel_grid, x_true), g, (0, A),
+                                cs.ProjectionMethod.INTERPOLATED)
+    pool = cs.DevicePool.b200(1)
+    tv = cs.TvParams(cs.TvMinimizer.GRADIENT_DESCENT, 1, 20, 1e-3)
+
+    def resid(v):
+        ax = cs.forward_project_slab(cs.Volume(g.voxel_grid, v), g, (0, A),
+                                     cs.ProjectionMethod.INTERPOLATED).data
+        return float((ax - b.data).double().norm() / b.data.double().norm())
+
+    out = {"measure": "c4_loops", "n": n, "views": A, "block": block}
+    for name, fn in (
+            ("sart_tv", lambda it: cs.os_sart(b, g, cs.ReconConfig(
+                pool, cs.Algorithm.OSSART, it, block, tv=tv)).data),
+            ("cgls", lambda it: cs.cgls(b, g, cs.ReconConfig(
+                pool, cs.Algorithm.CGLS, it)).volume.data)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fn(1)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        x = fn(1 + iters)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        out[name] = {"s_per_iter": (t2 - t1 - (t1 - t0)) / iters,
+                     "setup_plus_1iter_s": t1 - t0,
+                     "rel_residual_after": resid(x)}
+        del x
+        torch.cuda.empty_cache()
+    print(json.dumps(out), flush=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1]
     args = [float(a) for a in sys.argv[2:]]
@@ -240,5 +283,7 @@ if __name__ == "__main__":
         c3(*[int(a) for a in args])
     elif what == "c5":
         c5(*[int(a) for a in args])
+    elif what == "c4":
+        c4(*[int(a) for a in args])
     else:
         ooc(*([int(args[0])] if args else []) + ([int(args[1])] if len(args) > 1 else []) + (args[2:3]))
