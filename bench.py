@@ -463,15 +463,17 @@ def run_extras(args, cs, K, g, vol, y, dev, rank, world, arange, zrange):
     out["atb_matched_dense_gups"] = float(A) * (z1 - z0) * n * n / (
         s.elapsed_time(e) * 1e-3) / 1e9
     del dense
-    # TV-GD iteration (Sigma g^2 pass + step pass) and ROF dual iteration on
-    # the 512^3 volume (12 / 28 B per voxel-iteration)
+    # TV-GD iteration as the loops run it (g + Sigma g^2 pass, streaming
+    # step pass) and ROF dual iteration on the 512^3 volume (SURVEY 8(d):
+    # 12 / 28 B per voxel-iteration algorithmic)
     u2 = torch.empty_like(vol)
+    g2 = torch.empty_like(vol)
     ss = torch.zeros(1, dtype=torch.float64, device=dev)
     p3 = torch.zeros((3,) + tuple(vol.shape), device=dev)
     q3 = torch.empty_like(p3)
     for name, fn, bpv in (
-            ("tv_gd", lambda: (K.tv_grad_sumsq(vol, (0, n), ss),
-                               K.tv_step(vol, u2, 1e-3, ss, 1.0)), 12.0),
+            ("tv_gd", lambda: (K.tv_grad_store(vol, g2, (0, n), ss),
+                               K.tv_step_g(vol, g2, u2, 1e-3, ss, 1.0)), 12.0),
             ("tv_rof", lambda: K.rof_iter(vol, p3, q3, 0.1), 28.0)):
         fn()
         torch.cuda.synchronize()

@@ -138,6 +138,18 @@ int cs_tv_step(const float* u, float* u_out, int nx, int ny, int nzw,
                double step, const double* norm_sumsq_dev, double scale,
                cs_stream_t stream);
 
+/* The GD iteration in two passes that share g: g stored over the whole
+ * window (g[nzw][ny][nx], device) with Σg² over the core into out_sum, then
+ * u_out = u - step * g / (sqrt(*norm_sumsq_dev) * scale) elementwise over
+ * n voxels -- bit-identical to cs_tv_grad_sumsq + cs_tv_step, with the
+ * second pass a stream instead of a second stencil. */
+int cs_tv_grad_store(const float* u, float* g, int nx, int ny, int nzw,
+                     int core_lo, int core_hi, double* out_sum,
+                     cs_stream_t stream);
+int cs_tv_step_g(const float* u, const float* g, float* u_out, int64_t n,
+                 double step, const double* norm_sumsq_dev, double scale,
+                 cs_stream_t stream);
+
 /* One Chambolle dual iteration (regularization.py:174-182):
  *   u = f + lam div p; p += (1/12/lam) ∇u; p /= max(1, |p|)
  * p_in/p_out device [3][nzw][ny][nx] (must not alias). */

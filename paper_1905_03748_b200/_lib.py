@@ -48,6 +48,8 @@ SYMBOLS: dict[str, list] = {
     "cs_ray_table": [I, I, I, P, P, I, I, I, D, P, P, P, P],
     "cs_tv_grad_sumsq": [P, I, I, I, I, I, P, P],
     "cs_tv_grad_norm": [P, I, I, I, I, I, P, P],
+    "cs_tv_grad_store": [P, P, I, I, I, I, I, P, P],
+    "cs_tv_step_g": [P, P, P, L, D, P, D, P],
     "cs_tv_step": [P, P, I, I, I, D, P, D, P],
     "cs_rof_iter": [P, P, P, I, I, I, D, P],
     "cs_rof_finish": [P, P, P, I, I, I, D, P],

@@ -12,6 +12,7 @@
 // and writes u - step g / ||g|| to a second buffer; both are the tiled
 // kernel below.  ROF is one fused pass per iteration (28 B /
 // voxel-iteration) with neighbours through L1 (__ldg).
+#include <cstdint>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -79,12 +80,15 @@ constexpr int TV_TX = 32, TV_TY = 8, TV_ZC = 16;
 constexpr int TV_UX = TV_TX + 2, TV_UY = TV_TY + 2;  // u tile: x0-1 .. x0+32
 constexpr int TV_PX = TV_TX + 1, TV_PY = TV_TY + 1;  // p tile: x0-1 .. x0+31
 
-template <int PASS>  // 0: sum of g^2 over [z_begin, z_end); 1: step
+// PASS 0: sum of g^2 over [z_begin, z_end); 1: step; 2: g stored to uo
+// over [z_begin, z_end) and g^2 summed over the core [c_lo, c_hi)
+template <int PASS>
 __global__ void __launch_bounds__(TV_TX * TV_TY)
     tv_gd_tiled_kernel(const float* __restrict__ u, float* __restrict__ uo,
                        Win W, int z_begin, int z_end, double step,
                        const double* __restrict__ sumsq, double scale,
-                       double* __restrict__ partial) {
+                       double* __restrict__ partial, int c_lo = 0,
+                       int c_hi = 0) {
   constexpr int NT = TV_TX * TV_TY;
   constexpr int UN = TV_UX * TV_UY;            // 340 u values per plane
   constexpr int UPT = (UN + NT - 1) / NT;      // per thread (2)
@@ -198,6 +202,9 @@ __global__ void __launch_bounds__(TV_TX * TV_TY)
                         (spx[c_p] - spx[c_p - 1]));
       if (PASS == 0) {
         acc += (double)g * (double)g;
+      } else if (PASS == 2) {
+        uo[(size_t)z * plane + own_off] = g;
+        if (z >= c_lo && z < c_hi) acc += (double)g * (double)g;
       } else {
         const float uc = pl0[c_u];
         uo[(size_t)z * plane + own_off] =
@@ -210,7 +217,7 @@ __global__ void __launch_bounds__(TV_TX * TV_TY)
     pl1 = pl2;
     pl2 = t;
   }
-  if (PASS == 0) {
+  if (PASS != 1) {
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((tid & 31) == 0) sred[tid >> 5] = acc;
     __syncthreads();
@@ -339,6 +346,47 @@ int reduce_into(const double* partial, size_t n, double* out,
 
 __global__ void sqrt_in_place_kernel(double* v) { *v = sqrt(*v); }
 
+// u_out = u - step g / ||g|| from a stored g (cs_tv_grad_store): the same
+// fp64 update as tv_gd_tiled_kernel<1>, so results are bit-identical.
+__global__ void __launch_bounds__(256)
+    tv_step_g_kernel(const float4* __restrict__ u,
+                     const float4* __restrict__ g, float4* __restrict__ uo,
+                     size_t n4, double step, const double* __restrict__ sumsq,
+                     double scale) {
+  const double norm = sqrt(*sumsq) * scale;
+  const bool skip = norm < 1e-30;  // regularization.py:148-149
+  const double coef = skip ? 0.0 : step / norm;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const float4 a = __ldg(u + i);
+    if (skip) {
+      uo[i] = a;
+      continue;
+    }
+    const float4 b = __ldg(g + i);
+    float4 r;
+    r.x = (float)((double)a.x - coef * (double)b.x);
+    r.y = (float)((double)a.y - coef * (double)b.y);
+    r.z = (float)((double)a.z - coef * (double)b.z);
+    r.w = (float)((double)a.w - coef * (double)b.w);
+    uo[i] = r;
+  }
+}
+
+__global__ void tv_step_g_tail_kernel(const float* __restrict__ u,
+                                      const float* __restrict__ g,
+                                      float* __restrict__ uo, size_t i0,
+                                      size_t n, double step,
+                                      const double* __restrict__ sumsq,
+                                      double scale) {
+  const double norm = sqrt(*sumsq) * scale;
+  const bool skip = norm < 1e-30;
+  const double coef = skip ? 0.0 : step / norm;
+  const size_t i = i0 + threadIdx.x;
+  if (i < n)
+    uo[i] = skip ? u[i] : (float)((double)u[i] - coef * (double)g[i]);
+}
+
 static int check_win(int nx, int ny, int nzw) {
   CS_REQUIRE(nx >= 2 && ny >= 2 && nzw >= 2, CS_ERR_ARG,
              "TV needs at least 2 voxels per axis (got %d x %d x %d)", nx, ny,
@@ -399,6 +447,62 @@ int cs_tv_step(const float* u, float* u_out, int nx, int ny, int nzw,
       nullptr);
   CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
+  return CS_OK;
+}
+
+int cs_tv_grad_store(const float* u, float* g, int nx, int ny, int nzw,
+                     int core_lo, int core_hi, double* out_sum,
+                     cs_stream_t stream) {
+  int rc = check_win(nx, ny, nzw);
+  if (rc) return rc;
+  CS_REQUIRE(0 <= core_lo && core_lo < core_hi && core_hi <= nzw, CS_ERR_ARG,
+             "bad core [%d, %d) in window of %d", core_lo, core_hi, nzw);
+  CS_REQUIRE(u != g, CS_ERR_ARG, "cs_tv_grad_store: g aliases u");
+  cudaStream_t s = (cudaStream_t)stream;
+  const dim3 grid((nx + TV_TX - 1) / TV_TX, (ny + TV_TY - 1) / TV_TY,
+                  (nzw + TV_ZC - 1) / TV_ZC);
+  const size_t nb = (size_t)grid.x * grid.y * grid.z;
+  double* part = nullptr;
+  retain_pool();
+  CS_CHECK_CUDA(cudaMallocAsync((void**)&part, nb * sizeof(double), s));
+  tv_gd_tiled_kernel<2><<<grid, dim3(TV_TX, TV_TY), 0, s>>>(
+      u, g, Win{nx, ny, nzw}, 0, nzw, 0.0, nullptr, 1.0, part, core_lo,
+      core_hi);
+  CS_COUNT_LAUNCH();
+  CS_CHECK_CUDA(cudaGetLastError());
+  rc = reduce_into(part, nb, out_sum, s);
+  cudaFreeAsync(part, s);
+  return rc;
+}
+
+int cs_tv_step_g(const float* u, const float* g, float* u_out, int64_t n,
+                 double step, const double* norm_sumsq_dev, double scale,
+                 cs_stream_t stream) {
+  CS_REQUIRE(n >= 0, CS_ERR_ARG, "negative length");
+  CS_REQUIRE(u != u_out && g != u_out, CS_ERR_ARG,
+             "cs_tv_step_g: u_out aliases an input");
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool vec = ((uintptr_t)u % 16 == 0) && ((uintptr_t)g % 16 == 0) &&
+                   ((uintptr_t)u_out % 16 == 0);
+  size_t n4 = vec ? (size_t)n / 4 : 0;
+  if (n4) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t want = (n4 + 255) / 256;
+    const unsigned blocks = (unsigned)(want < (size_t)sms * 16 ? want : (size_t)sms * 16);
+    tv_step_g_kernel<<<blocks, 256, 0, s>>>(
+        reinterpret_cast<const float4*>(u), reinterpret_cast<const float4*>(g),
+        reinterpret_cast<float4*>(u_out), n4, step, norm_sumsq_dev, scale);
+    CS_COUNT_LAUNCH();
+    CS_CHECK_CUDA(cudaGetLastError());
+  }
+  for (size_t i0 = n4 * 4; i0 < (size_t)n; i0 += 1024) {
+    tv_step_g_tail_kernel<<<1, 1024, 0, s>>>(u, g, u_out, i0, (size_t)n, step,
+                                             norm_sumsq_dev, scale);
+    CS_COUNT_LAUNCH();
+    CS_CHECK_CUDA(cudaGetLastError());
+  }
   return CS_OK;
 }
 

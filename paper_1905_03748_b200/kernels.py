@@ -200,6 +200,27 @@ def tv_grad_sumsq(u: torch.Tensor, core, out: torch.Tensor, stream=None):
     return out
 
 
+def tv_grad_store(u: torch.Tensor, g: torch.Tensor, core, out: torch.Tensor,
+                  stream=None):
+    """g = TV subgradient over the whole window; out[0] = Σg² over the
+    core planes (the first pass of a GD iteration, g kept for the step)."""
+    nz, ny, nx = u.shape
+    check(lib().cs_tv_grad_store(dptr(_f32(u, "u")), dptr(_f32(g, "g")), nx,
+                                 ny, nz, core[0], core[1], dptr(out),
+                                 stream_ptr(stream)))
+    return g
+
+
+def tv_step_g(u: torch.Tensor, g: torch.Tensor, u_out: torch.Tensor,
+              step: float, sumsq: torch.Tensor, scale: float = 1.0,
+              stream=None):
+    """u_out = u - step g / (sqrt(sumsq) scale) (bit-identical to tv_step)."""
+    check(lib().cs_tv_step_g(dptr(_f32(u, "u")), dptr(_f32(g, "g")),
+                             dptr(_f32(u_out, "u_out")), u.numel(), step,
+                             dptr(sumsq), scale, stream_ptr(stream)))
+    return u_out
+
+
 def tv_grad_norm(u: torch.Tensor, core, out: torch.Tensor, stream=None):
     """out[0] = ||g||_2 over the core planes (regularization.py:147)."""
     nz, ny, nx = u.shape

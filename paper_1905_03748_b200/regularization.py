@@ -125,10 +125,11 @@ def _gd_iterations(u: torch.Tensor, iters: int, step: float) -> torch.Tensor:
     nz = u.shape[0]
     a = u.clone()
     b = torch.empty_like(a)
+    g = torch.empty_like(a)  # g kept between the passes: the step streams
     ss = _scalar(a.device)
     for _ in range(iters):
-        K.tv_grad_sumsq(a, (0, nz), ss)
-        K.tv_step(a, b, step, ss, 1.0)
+        K.tv_grad_store(a, g, (0, nz), ss)
+        K.tv_step_g(a, g, b, step, ss, 1.0)
         a, b = b, a
     return a
 
@@ -236,18 +237,21 @@ def _split_gd(u0: torch.Tensor, slabs: list[HaloSlab],
         snap = u.clone()  # halo exchange: ghosts become neighbour cores
         local = [snap[s.window[0]:s.window[1]].clone() for s in slabs]
         spare = [torch.empty_like(w) for w in local]
+        gs = [torch.empty_like(w) for w in local]
         for _ in range(params.inner_iters):
             for i, (s, w) in enumerate(zip(slabs, local)):
                 core = s.core_in_window if exact else slice(0, w.shape[0])
-                K.tv_grad_sumsq(w, (core.start, core.stop), sums[i:i + 1])
+                K.tv_grad_store(w, gs[i], (core.start, core.stop),
+                                sums[i:i + 1])
             if exact:
                 tot = sums.sum().reshape(1)
                 for i, w in enumerate(local):
-                    K.tv_step(w, spare[i], params.step, tot, 1.0)
+                    K.tv_step_g(w, gs[i], spare[i], params.step, tot, 1.0)
             else:
                 for i, w in enumerate(local):
                     scale = float(np.sqrt(total_voxels / w.numel()))
-                    K.tv_step(w, spare[i], params.step, sums[i:i + 1], scale)
+                    K.tv_step_g(w, gs[i], spare[i], params.step,
+                                sums[i:i + 1], scale)
             local, spare = spare, local
         for s, w in zip(slabs, local):
             u[s.core_range[0]:s.core_range[1]] = w[s.core_in_window]

@@ -727,3 +727,29 @@ def test_tv_grad_norm_and_sumsq_vs_oracle(golden):
     K.tv_grad_sumsq(ud, (5, 17), out)
     ref2 = float((g[5:17] ** 2).sum())
     assert abs(float(out) - ref2) <= 2e-5 * ref2
+
+
+def test_tv_stored_g_pair_bit_identical():
+    """cs_tv_grad_store + cs_tv_step_g (the production GD iteration) give
+    exactly the bits of cs_tv_grad_sumsq + cs_tv_step over a whole window
+    (a core band: the same up to the grouping of the fp64 partial sums);
+    odd sizes exercise the scalar tail of the streaming step."""
+    import torch
+    from paper_1905_03748_b200 import kernels as K
+    u = torch.rand((13, 11, 9), device="cuda")
+    for core in ((0, 13), (3, 10)):
+        s1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        s2 = torch.zeros_like(s1)
+        K.tv_grad_sumsq(u, core, s1)
+        o1 = torch.empty_like(u)
+        K.tv_step(u, o1, 0.05, s1, 1.3)
+        g = torch.empty_like(u)
+        K.tv_grad_store(u, g, core, s2)
+        o2 = torch.empty_like(u)
+        K.tv_step_g(u, g, o2, 0.05, s2, 1.3)
+        if core == (0, 13):
+            assert torch.equal(s1, s2)
+            assert torch.equal(o1, o2)
+        else:  # the core's fp64 partials are grouped differently
+            assert abs(float(s1) - float(s2)) <= 1e-12 * float(s1)
+            assert torch.allclose(o1, o2, rtol=1e-6, atol=1e-7)

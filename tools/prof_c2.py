@@ -23,14 +23,15 @@ K.fwd_interp(vol, g, (0, A), (0, n), y)
 acc = torch.zeros((n, n, n), device=dev)
 proj = torch.empty((C, n, n), device=dev)
 u2 = torch.empty_like(vol)
+g2 = torch.empty_like(vol)
 ss = torch.zeros(1, dtype=torch.float64, device=dev)
 p3 = torch.zeros((3, n, n, n), device=dev)
 q3 = torch.empty_like(p3)
 torch.cuda.synchronize()
 for rep in range(2):
     if "tv" in which:
-        K.tv_grad_sumsq(vol, (0, n), ss)
-        K.tv_step(vol, u2, 1e-3, ss, 1.0)
+        K.tv_grad_store(vol, g2, (0, n), ss)
+        K.tv_step_g(vol, g2, u2, 1e-3, ss, 1.0)
         K.rof_iter(vol, p3, q3, 0.1)
     if "fwd" in which:
         K.fwd_interp(vol, g, (0, C), (0, n), proj)

@@ -31,13 +31,14 @@ ops = {
 only = os.environ.get("PROF_ONLY")
 if not only or "tv_gd_iter" in only or "rof_iter" in only:
     u2 = torch.empty_like(vol)
+    g2 = torch.empty_like(vol)
     ss = torch.zeros(1, dtype=torch.float64, device=dev)
     p3 = torch.zeros((3, n, n, n), device=dev)
     q3 = torch.empty_like(p3)
 
     def tv_gd():
-        K.tv_grad_sumsq(vol, (0, n), ss)
-        K.tv_step(vol, u2, 1e-3, ss, 1.0)
+        K.tv_grad_store(vol, g2, (0, n), ss)
+        K.tv_step_g(vol, g2, u2, 1e-3, ss, 1.0)
 
     ops["tv_gd_iter"] = tv_gd
     ops["rof_iter"] = lambda: K.rof_iter(vol, p3, q3, 0.1)
