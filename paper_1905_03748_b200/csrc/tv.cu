@@ -8,9 +8,11 @@
 //   -(pz(i) - pz(i - ez) + py(i) - py(i - ey) + px(i) - px(i - ex)).
 // GD needs the global norm of g before the update, so it is two passes
 // (12 B / voxel-iteration): pass 1 reduces Σg² over the core
-// planes in fp64 (deterministic two-stage reduction), pass 2 recomputes g
-// and writes u - step g / ||g|| to a second buffer; both are the tiled
-// kernel below.  ROF is one fused pass per iteration (28 B /
+// planes in fp64 (deterministic two-stage reduction), pass 2 writes
+// u - step g / ||g|| to a second buffer.  Production (cs_tv_grad_store +
+// cs_tv_step_g): pass 1 also stores g and pass 2 is a float4 stream
+// (147 vs 113 Gvox*it/s at 512^3 with pass 2 recomputing g, which
+// cs_tv_grad_sumsq + cs_tv_step still do).  ROF is one fused pass per iteration (28 B /
 // voxel-iteration) with neighbours through L1 (__ldg).
 #include <cstdint>
 #include <cstdlib>
