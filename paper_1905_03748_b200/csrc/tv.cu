@@ -302,11 +302,13 @@ __global__ void __launch_bounds__(256)
   float qz = __ldg(pi) + tau_over_lam * gz;
   float qy = __ldg(pi + vol) + tau_over_lam * gy;
   float qx = __ldg(pi + 2 * vol) + tau_over_lam * gx;
-  const float mag = fmaxf(sqrtf(qz * qz + qy * qy + qx * qx), 1.f);
+  // p / max(1, |p|): one reciprocal (mag >= 1) instead of three IEEE
+  // divisions
+  const float inv = __frcp_rn(fmaxf(sqrtf(qz * qz + qy * qy + qx * qx), 1.f));
   float* po = pout + i;
-  po[0] = qz / mag;
-  po[vol] = qy / mag;
-  po[2 * vol] = qx / mag;
+  po[0] = qz * inv;
+  po[vol] = qy * inv;
+  po[2 * vol] = qx * inv;
 }
 
 __global__ void __launch_bounds__(256)
