@@ -224,6 +224,9 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
   // extents are reduced in one pass), and only then served from global.
   int k = k0;
   int cur = dir > 0 ? mlo : mhi;  // next M-cell in march order
+  // reciprocal of the M step for the chunk-end estimates (an estimate:
+  // the exact cell test settles it), one division per ray
+  const float rbm = has ? 1.f / m.B[M] : 0.f;
   const bool run = !mixed;
   while (run && (dir > 0 ? cur <= mhi : cur >= mlo)) {
     // candidate chunks: S = ST_S (index 0) and ST_S / 2 (index 1)
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
         // k* = kc + (face - A_M) / B_M; estimate, then settle on the exact
         // fp32 cell test (the same floor the sampling loop uses)
         const float face = dir > 0 ? (float)(c_hi + 1) : (float)c_lo;
-        const float kst = (face - m.A[M]) / m.B[M] + (float)(int)m.kc;
+        const float kst = (face - m.A[M]) * rbm + (float)(int)m.kc;
         int ke = (int)fminf(fmaxf(ceilf(kst), (float)k), (float)k1);
         if (dir > 0) {
           while (ke > k && qfloor(m, ke - 1, M) > c_hi) ke--;
