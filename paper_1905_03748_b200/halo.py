@@ -28,6 +28,9 @@ class CudaTvOps:
 
     grad_sumsq = staticmethod(K.tv_grad_sumsq)
     step = staticmethod(K.tv_step)
+    # the GD pair the loops use: g kept between the passes (bit-identical)
+    grad_store = staticmethod(K.tv_grad_store)
+    step_g = staticmethod(K.tv_step_g)
     rof_iter = staticmethod(K.rof_iter)
     rof_finish = staticmethod(K.rof_finish)
 
@@ -118,16 +121,23 @@ def split_minimize_distributed(u_full: torch.Tensor, slabs, params, rank: int,
         ss = torch.zeros(1, dtype=torch.float64, device=w.device)
         exact = params.norm_mode is NormMode.EXACT_GLOBAL
         scale = 1.0 if exact else float(np.sqrt(total_voxels / w.numel()))
+        stored = hasattr(ops, "grad_store")
+        g = torch.empty_like(w) if stored else None
         for epoch in range(params.outer_syncs):
             if epoch > 0:
                 exchange_halos(w, slabs, rank)
             for _ in range(params.inner_iters):
-                if exact:
-                    ops.grad_sumsq(w, (core.start, core.stop), ss)
-                    dist.all_reduce(ss)
+                band = (core.start, core.stop) if exact else (0, w.shape[0])
+                if stored:
+                    ops.grad_store(w, g, band, ss)
                 else:
-                    ops.grad_sumsq(w, (0, w.shape[0]), ss)
-                ops.step(w, spare, params.step, ss, scale)
+                    ops.grad_sumsq(w, band, ss)
+                if exact:
+                    dist.all_reduce(ss)
+                if stored:
+                    ops.step_g(w, g, spare, params.step, ss, scale)
+                else:
+                    ops.step(w, spare, params.step, ss, scale)
                 w, spare = spare, w
         return gather_cores(w, slabs, rank, tuple(u_full.shape))
     f = u_full

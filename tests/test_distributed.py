@@ -99,15 +99,34 @@ class CpuTvOps:
         u.copy_(f.double() + lam * _div(p64[0], p64[1], p64[2]))
 
 
-def _tv_worker(rank, world, port, f, params_kw, q):
+class CpuTvOpsStored(CpuTvOps):
+    """Adds the stored-g GD pair (CudaTvOps.grad_store / step_g)."""
+
+    @staticmethod
+    def grad_store(w, g, core, out):
+        g.copy_(_subgrad(w.double()))
+        gc = g.double()[core[0]:core[1]]
+        out[0] = (gc * gc).sum()
+
+    @staticmethod
+    def step_g(w, g, out, step, ss, scale):
+        norm = float(np.sqrt(float(ss[0]))) * scale
+        if norm < 1e-30:
+            out.copy_(w)
+        else:
+            out.copy_(w.double() - step * g.double() / norm)
+
+
+def _tv_worker(rank, world, port, f, params_kw, q, stored=False):
     _init(rank, world, port)
     from paper_1905_03748_b200 import halo
     from paper_1905_03748_b200.regularization import (TvParams,
                                                       make_halo_slabs)
     params = TvParams(**params_kw)
     slabs = make_halo_slabs(f.shape[0], world, params.effective_halo())
-    out = halo.split_minimize_distributed(torch.from_numpy(f), slabs, params,
-                                          rank, ops=CpuTvOps)
+    out = halo.split_minimize_distributed(
+        torch.from_numpy(f), slabs, params, rank,
+        ops=CpuTvOpsStored if stored else CpuTvOps)
     if rank == 0:
         q.put(out.numpy())
     dist.barrier()
@@ -130,7 +149,8 @@ def _run(fn, world, *args):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("case", ["gd_exact", "gd_local", "rof"])
+@pytest.mark.parametrize("case", ["gd_exact", "gd_local", "rof",
+                                  "gd_exact_stored", "gd_local_stored"])
 def test_distributed_tv_split_matches_oracle(world, case):
     from paper_1905_03748_b200.regularization import NormMode, TvMinimizer
     from oracle import oracle as O
@@ -143,16 +163,23 @@ def test_distributed_tv_split_matches_oracle(world, case):
                   lam=0.1, halo_depth=4)
         ref = O.split_minimize(f, world, "rof", 3, 3, lam=0.1, halo=4)
     else:
-        exact = case == "gd_exact"
+        exact = case.startswith("gd_exact")
         kw = dict(minimizer=TvMinimizer.GRADIENT_DESCENT, outer_syncs=3,
                   inner_iters=3, step=0.05, halo_depth=4,
                   norm_mode=NormMode.EXACT_GLOBAL if exact
                   else NormMode.LOCAL_APPROX)
         ref = O.split_minimize(f, world, "gd", 3, 3, step=0.05,
                                exact_global=exact, halo=4)
-    got = _run(_tv_worker, world, f, kw)
+    if case.endswith("_stored"):
+        got = _run(_tv_worker_stored, world, f, kw)
+    else:
+        got = _run(_tv_worker, world, f, kw)
     err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     assert err < 1e-6, err
+
+
+def _tv_worker_stored(rank, world, port, f, params_kw, q):
+    _tv_worker(rank, world, port, f, params_kw, q, stored=True)
 
 
 def _gather_worker(rank, world, port, q):
