@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
   // tile corners (voxel centres) for the footprint boxes
   const int xl = min(bx0 + FS_TX, nx) - 1, yl = min(by0 + FS_TY, ny) - 1;
   const int zl = min(zb + FDK_ZB, n_slab) - 1;
+  const int nk = zl - zb + 1;  // planes of this CTA inside the slab
   const double cxs[2] = {gx0 + (bx0 + 0.5) * vx, gx0 + (xl + 0.5) * vx};
   const double cys[2] = {gy0 + (by0 + 0.5) * vy, gy0 + (yl + 0.5) * vy};
   const double czs[2] = {wz0, gz0 + (z_lo + zl + 0.5) * vz};
@@ -230,8 +231,7 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
           const int col = (int)fu0 - b.u0;
           const int row0 = (int)fv0 - b.v0;
           const float* base = sbox + b.off + col;
-#pragma unroll
-          for (int k = 0; k < FDK_ZB; k++) {
+          auto tap = [&](int k) {
             const float vv = fmaf((float)k, dvz, vfrac);
             const float fl = floorf(vv);
             const float fv = vv - fl;
@@ -243,6 +243,17 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
             const float r0 = fmaf(fu, t01 - t00, t00);
             const float r1 = fmaf(fu, t11 - t10, t10);
             acc[k] = fmaf(w2, fmaf(fv, r1 - r0, r0), acc[k]);
+          };
+          if (nk == FDK_ZB) {
+#pragma unroll
+            for (int k = 0; k < FDK_ZB; k++) tap(k);
+          } else {
+            // the slab's last z-block: planes past the slab lie outside the
+            // staged footprint (its z range is the slab's), so they are
+            // not sampled (CTA-uniform branch)
+#pragma unroll
+            for (int k = 0; k < FDK_ZB; k++)
+              if (k < nk) tap(k);
           }
         }
       }

@@ -796,3 +796,26 @@ def test_randomised_geometries_vs_oracle():
                           (cs.WeightMode.FDK, O.bwd_fdk)):
             assert rel_l2(cs.backproject_slab(st, g, (z0, z1), mode).data,
                           ofn(y[a0:a1], og, (a0, a1), (z0, z1))) <= TOL_OP
+
+
+def test_fdk_thin_slab_fine_pixels_regression():
+    """Regression (found by tools/fuzz_parity.py with FUZZ_FINE): a 2-plane
+    slab under pixels ~6x finer than voxels -- the staged FDK read planes
+    past the slab outside its staged footprint (an illegal shared-memory
+    address); they are no longer sampled."""
+    grid = cs.VoxelGrid(38, 26, 28, (1.353254259269713, 0.7477279089896511,
+                                     0.830182913402348),
+                        (2.2413206723775714, -2.9684081726065514,
+                         1.9273705102965977))
+    det = cs.DetectorGrid(86, 35, (0.1323645593008397, 0.14701814799123764),
+                          (0.031064659895868055, 0.1651667141129686))
+    g = cs.ScanGeometry(109.23412942205707, 175.3939285422945,
+                        (6.937003968081498, 4.097266868992543,
+                         1.7105092121762766, 6.845442067546388), grid, det)
+    og = to_oracle(g)
+    y = np.random.default_rng(3).standard_normal((4, 35, 86)).astype(
+        np.float32)
+    for zr in ((26, 28), (0, 28), (5, 6)):
+        st = cs.ProjectionStack(det, y[2:3], (2, 3))
+        got = cs.backproject_slab(st, g, zr, cs.WeightMode.FDK).data
+        assert rel_l2(got, O.bwd_fdk(y[2:3], og, (2, 3), zr)) <= TOL_OP, zr

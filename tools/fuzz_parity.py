@@ -4,6 +4,7 @@ angle sets, slab and view windows; Ax (interp, Siddon), matched and FDK Atb.
 Prints one JSON line per failing case and a summary.
 
     python tools/fuzz_parity.py [cases=60] [seed=0]
+    FUZZ_FINE=0.5 python tools/fuzz_parity.py ...   # half with fine pixels
 """
 import json
 import math
@@ -19,6 +20,7 @@ from conftest import rel_l2, to_oracle
 from oracle import oracle as O
 
 IP, SD = cs.ProjectionMethod.INTERPOLATED, cs.ProjectionMethod.SIDDON
+FINE_FRACTION = float(os.environ.get("FUZZ_FINE", "0"))
 
 
 def case(rng):
@@ -29,10 +31,11 @@ def case(rng):
     r = grid.bounding_radius()
     dso = float(r * rng.uniform(1.3, 4.0) + abs(off[0]) + abs(off[1]) + 1.0)
     dsd = float(dso + r * rng.uniform(1.2, 3.0) + abs(off[0]) + abs(off[1]))
-    nu, nv = (int(v) for v in rng.integers(4, 48, 2))
+    fine = rng.random() < FINE_FRACTION  # pixels much finer than voxels
+    nu, nv = (int(v) for v in rng.integers(4, 96 if fine else 48, 2))
     ext = grid.extent
     mag = dsd / dso
-    span = rng.uniform(0.6, 1.6)
+    span = rng.uniform(0.6, 1.6) * (rng.uniform(0.05, 0.3) if fine else 1.0)
     pitch = (float(span * mag * max(ext[0], ext[1]) / nu),
              float(span * mag * ext[2] / nv))
     doff = (float(rng.uniform(-0.3, 0.3) * nu * pitch[0]),
@@ -64,6 +67,12 @@ def main():
         z1 = int(rng.integers(z0 + 1, nz + 1))
         a0 = int(rng.integers(0, na))
         a1 = int(rng.integers(a0 + 1, na + 1))
+        print(json.dumps({"start": i, "grid": [grid.n_x, grid.n_y, nz],
+                          "vox": grid.voxel_size, "off": grid.origin_offset,
+                          "dso": g.dso, "dsd": g.dsd, "angles": g.angles,
+                          "det": [det.n_u, det.n_v], "pitch": det.pixel_size,
+                          "det_off": det.detector_offset, "slab": [z0, z1],
+                          "views": [a0, a1]}), file=sys.stderr, flush=True)
         res = {}
         xs = x[z0:z1]
         res["ax"] = rel_l2(cs.forward_project_slab(
