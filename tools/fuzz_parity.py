@@ -5,6 +5,7 @@ Prints one JSON line per failing case and a summary.
 
     python tools/fuzz_parity.py [cases=60] [seed=0]
     FUZZ_FINE=0.5 python tools/fuzz_parity.py ...   # half with fine pixels
+    FUZZ_CLOSE=1 FUZZ_VIEWS=40 python tools/fuzz_parity.py ...  # wide fan
 """
 import json
 import math
@@ -21,6 +22,8 @@ from oracle import oracle as O
 
 IP, SD = cs.ProjectionMethod.INTERPOLATED, cs.ProjectionMethod.SIDDON
 FINE_FRACTION = float(os.environ.get("FUZZ_FINE", "0"))
+CLOSE = os.environ.get("FUZZ_CLOSE") == "1"
+MAX_VIEWS = int(os.environ.get("FUZZ_VIEWS", "12"))
 
 
 def case(rng):
@@ -29,7 +32,9 @@ def case(rng):
     off = tuple(float(v) for v in rng.uniform(-3, 3, 3))
     grid = cs.VoxelGrid(nx, ny, nz, vox, off)
     r = grid.bounding_radius()
-    dso = float(r * rng.uniform(1.3, 4.0) + abs(off[0]) + abs(off[1]) + 1.0)
+    lo = 1.05 if CLOSE else 1.3  # FUZZ_CLOSE: source near the grid (wide fan)
+    dso = float(r * rng.uniform(lo, 1.4 if CLOSE else 4.0) + abs(off[0])
+                + abs(off[1]) + 1.0)
     dsd = float(dso + r * rng.uniform(1.2, 3.0) + abs(off[0]) + abs(off[1]))
     fine = rng.random() < FINE_FRACTION  # pixels much finer than voxels
     nu, nv = (int(v) for v in rng.integers(4, 96 if fine else 48, 2))
@@ -40,7 +45,7 @@ def case(rng):
              float(span * mag * ext[2] / nv))
     doff = (float(rng.uniform(-0.3, 0.3) * nu * pitch[0]),
             float(rng.uniform(-0.3, 0.3) * nv * pitch[1]))
-    na = int(rng.integers(1, 13))
+    na = int(rng.integers(1, MAX_VIEWS + 1))
     angles = tuple(float(a) for a in rng.uniform(-7, 7, na))
     det = cs.DetectorGrid(nu, nv, pitch, doff)
     return cs.ScanGeometry(dso, dsd, angles, grid, det)
