@@ -226,7 +226,13 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
           const double fu0 = floor(uf), fv0 = floor(vf);
           const float fu = (float)(uf - fu0);
           const float vfrac = (float)(vf - fv0);
-          const float dvz = (float)(vz * mag * inv_dv);
+          // rows per plane split into integer rows + fraction, so the fp32
+          // walk only carries the fraction (fine pixels: ~9 rows per plane,
+          // ulp(16 x 9) would be 1.5e-5 of a row at the 16th plane)
+          const double dvd = vz * mag * inv_dv;
+          const double dvi = floor(dvd);
+          const int di = (int)dvi;
+          const float dvz = (float)(dvd - dvi);
           const FsBox b = sb[j];
           const int col = (int)fu0 - b.u0;
           const int row0 = (int)fv0 - b.v0;
@@ -236,7 +242,8 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
             const float fl = floorf(vv);
             const float fv = vv - fl;
             // integral fl, |fl| < 2^22: int via the 1.5 * 2^23 magic add
-            const int il = __float_as_int(fl + 12582912.f) - 0x4B400000;
+            const int il = __float_as_int(fl + 12582912.f) - 0x4B400000 +
+                           k * di;
             const float* q = base + (row0 + il) * b.nu;
             const float t00 = q[0], t01 = q[1];
             const float t10 = q[b.nu], t11 = q[b.nu + 1];
