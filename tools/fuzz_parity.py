@@ -24,10 +24,11 @@ IP, SD = cs.ProjectionMethod.INTERPOLATED, cs.ProjectionMethod.SIDDON
 FINE_FRACTION = float(os.environ.get("FUZZ_FINE", "0"))
 CLOSE = os.environ.get("FUZZ_CLOSE") == "1"
 MAX_VIEWS = int(os.environ.get("FUZZ_VIEWS", "12"))
+MAX_N = int(os.environ.get("FUZZ_MAXN", "40"))
 
 
 def case(rng):
-    nx, ny, nz = (int(v) for v in rng.integers(3, 41, 3))
+    nx, ny, nz = (int(v) for v in rng.integers(3, MAX_N + 1, 3))
     vox = tuple(float(v) for v in rng.uniform(0.5, 1.6, 3))
     off = tuple(float(v) for v in rng.uniform(-3, 3, 3))
     grid = cs.VoxelGrid(nx, ny, nz, vox, off)
