@@ -36,6 +36,9 @@ constexpr int ST_THREADS = ST_TU * ST_TV;
 #define CS_ST_S 8
 #endif
 constexpr int ST_S = CS_ST_S;  // planes per chunk along the main axis
+#ifndef ST_PRECISE_W
+#define ST_PRECISE_W 0.f  // corner-weight threshold of the fp32 global path
+#endif
 
 
 // Float -> int without the conversion pipe: for |x| < 2^22, x + 1.5 * 2^23
@@ -403,6 +406,35 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
             const float b0 = fmaf(wy, r01 - r00, r00);
             const float b1 = fmaf(wy, r11 - r10, r10);
             acc += fmaf(wz, b1 - b0, b0);
+          } else if (ST_PRECISE_W > 0.f &&
+                     fminf(fminf(fminf(wx, 1.f - wx), fminf(wy, 1.f - wy)),
+                           fminf(wz, 1.f - wz)) < ST_PRECISE_W) {
+            // a corner weight below ST_PRECISE_W: the box's fixed point
+            // (resolution 2.5e-7 of the CTA's largest tap) would cost such
+            // taps their relative accuracy, which voxels reached only by
+            // them (grid edges) need -- fp32 global atomics instead
+            const float t = val * (float)r.step;
+            const int ax = ix + bo[0], ay = iy + bo[1], az = iz + bo[2];
+#pragma unroll
+            for (int cz = 0; cz < 2; cz++) {
+              const int zi = az + cz;
+              if (zi < z_lo || zi >= z_hi) continue;
+              const float fz_ = cz ? wz : 1.f - wz;
+#pragma unroll
+              for (int cy = 0; cy < 2; cy++) {
+                const int yi = ay + cy;
+                if (yi < 0 || yi >= ny) continue;
+                const float fy_ = cy ? wy : 1.f - wy;
+#pragma unroll
+                for (int cx = 0; cx < 2; cx++) {
+                  const int xi = ax + cx;
+                  if (xi < 0 || xi >= nx) continue;
+                  atomicAdd(vol_acc + (size_t)(zi - z_lo) * plane +
+                                (size_t)yi * nx + xi,
+                            t * (fz_ * fy_ * (cx ? wx : 1.f - wx)));
+                }
+              }
+            }
           } else {
             const float z0 = sv * (1.f - wz), z1 = sv * wz;
             const float y00 = z0 * (1.f - wy), y01 = z0 * wy;
