@@ -47,3 +47,32 @@ got = cs.os_sart(cs.ProjectionStack(det, b), g, cs.ReconConfig(pool, cs.Algorith
 ref = O.os_sart(b, og, its, block, lam)
 print("os_sart relL2", rel_l2(got, ref))
 d = np.abs(got - ref); j = np.argmax(d); print("worst voxel", np.unravel_index(j, d.shape), got.ravel()[j], ref.ravel()[j], "col_o", col_o.ravel()[j])
+
+# hypothesis test: OS-SART with the GPU operators but V (and W) from fp64
+def blocks_of(na, bs):
+    return O.angle_blocks(na, bs)
+
+def sart(Vsrc):
+    xg = np.zeros((grid.n_z, grid.n_y, grid.n_x), np.float64)
+    bl = blocks_of(na, block)
+    for _ in range(its):
+        for (b0, b1) in bl:
+            xt = torch.from_numpy(xg.astype(np.float32)).to(dev)
+            ax = torch.empty((b1 - b0, det.n_v, det.n_u), device=dev)
+            K.fwd_interp(xt, g, (b0, b1), (0, grid.n_z), ax)
+            rowb = O.fwd_interp(ones, og, (b0, b1)).astype(np.float64)
+            W = O.guarded_inverse(rowb)
+            resid = (b[b0:b1].astype(np.float64) - ax.cpu().numpy()) * W
+            acc = torch.zeros((grid.n_z, grid.n_y, grid.n_x), device=dev)
+            K.bwd_matched(torch.from_numpy(resid.astype(np.float32)).to(dev), g, (b0, b1), (0, grid.n_z), acc)
+            if Vsrc == "oracle":
+                colb = O.bwd_matched(np.ones((b1 - b0, det.n_v, det.n_u), np.float32), og, (b0, b1)).astype(np.float64)
+            else:
+                cb = torch.zeros((grid.n_z, grid.n_y, grid.n_x), device=dev)
+                K.bwd_matched(torch.ones((b1 - b0, det.n_v, det.n_u), device=dev), g, (b0, b1), (0, grid.n_z), cb)
+                colb = cb.cpu().numpy().astype(np.float64)
+            V = O.guarded_inverse(colb)
+            xg += lam * V * acc.cpu().numpy()
+    return xg.astype(np.float32)
+
+print("emulated, V gpu:", rel_l2(sart("gpu"), ref), " V oracle:", rel_l2(sart("oracle"), ref))
