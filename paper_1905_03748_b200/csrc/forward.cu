@@ -562,7 +562,7 @@ static int launch_interp(const float* vol, int nx, int ny, int nz, int z_lo,
     // nothing was launched for a sub-slab whose array failed: retry it
     // smaller (not the residual epilogue, which needs the whole slab)
     if (rc == CS_ERR_CUDA && strstr(cs_last_error(), "out of memory") &&
-        MODE != FWD_RESIDUAL && h > 8) {
+        MODE != FWD_RESIDUAL && h > 1) {
       h = (h + 1) / 2;
       continue;
     }
