@@ -183,6 +183,11 @@ int cs_guarded_inverse(const float* a, float* out, int64_t n,
 /* x += lam * v * upd; upd = 0  (algorithms.py:298 + buffer reset) */
 int cs_sart_update(float* x, float* upd, const float* v, double lam,
                    int64_t n, cs_stream_t stream);
+/* r = w * (b - r) (w may be NULL: r = b - r) -- OS-SART's weighted
+ * residual W_S (b_S - A_S x) on a projection shard (algorithms.py:296-297)
+ * when A_S x arrives from the slab-sharded forward pass */
+int cs_weighted_residual(float* r, const float* b, const float* w, int64_t n,
+                         cs_stream_t stream);
 /* x = value */
 int cs_fill(float* x, float value, int64_t n, cs_stream_t stream);
 

@@ -25,7 +25,11 @@ class NativeLibraryError(RuntimeError):
 
 
 class ConesplitCudaError(RuntimeError):
-    """A C-ABI call returned an error code."""
+    """A C-ABI call returned an error code (``code``: CS_ERR_*)."""
+
+    def __init__(self, msg: str, code: int = 0):
+        super().__init__(msg)
+        self.code = code
 
 
 P = ctypes.c_void_p
@@ -59,6 +63,7 @@ SYMBOLS: dict[str, list] = {
     "cs_xpay_ratio": [P, P, L, P, P, P],
     "cs_guarded_inverse": [P, P, L, P],
     "cs_sart_update": [P, P, P, D, L, P],
+    "cs_weighted_residual": [P, P, P, L, P],
     "cs_fill": [P, ctypes.c_float, L, P],
 }
 
@@ -100,7 +105,7 @@ def lib() -> ctypes.CDLL:
 def check(rc: int) -> None:
     if rc != 0:
         msg = _lib.cs_last_error().decode() if _lib is not None else "?"
-        raise ConesplitCudaError(f"conesplit_b200 error {rc}: {msg}")
+        raise ConesplitCudaError(f"conesplit_b200 error {rc}: {msg}", rc)
 
 
 def dptr(t) -> int:

@@ -16,7 +16,13 @@
 //     with native int32 shared atomics (ATOMS.ADD; fp32 shared atomics are
 //     CAS loops on sm_100) in fixed point, scaled per CTA by its largest
 //     |proj| so no voxel sum can overflow; the box is then added to global
-//     memory with one 16-byte RED per aligned x-quad.
+//     memory with one 16-byte RED per aligned x-quad.  Where a voxel can
+//     be reached only by tiny trilinear weights -- CTAs at the detector
+//     border, and chunks where neighbouring rays are >= CS_ST_PRECISE_FP
+//     voxels apart -- the chunk's box holds two words per voxel: the tap
+//     rounded to the CTA's unit plus its exact rounding residual at 2^-k
+//     of that unit ("precise" boxes), so tiny sums keep their relative
+//     accuracy (the reference accumulates in fp64, _kernels.py:278-337).
 // Samples, weights and masks are exactly those of the texture kernel (same
 // fp64 ray set-up, same exact fixed-point positions q(k) = A0 + k Bq), so
 // chunking changes only summation order.  Boxes that would not fit the
@@ -36,9 +42,6 @@ constexpr int ST_THREADS = ST_TU * ST_TV;
 #define CS_ST_S 8
 #endif
 constexpr int ST_S = CS_ST_S;  // planes per chunk along the main axis
-#ifndef ST_PRECISE_W
-#define ST_PRECISE_W 0.f  // corner-weight threshold of the fp32 global path
-#endif
 
 
 // Float -> int without the conversion pipe: for |x| < 2^22, x + 1.5 * 2^23
@@ -64,16 +67,23 @@ __device__ __forceinline__ void st_red4(float* p, float a, float b, float c,
                : "memory");
 }
 
-// WIDE (matched only): int64 box accumulators.  The int32 box must keep
-// every per-voxel chunk sum below 2^31, so its fixed-point scale shrinks
-// when many rays cross a voxel (detector pixels much finer than voxels:
-// fixed_point_budget); there the 64-bit box keeps the full 2^-22-of-max-tap
-// resolution at twice the shared memory per entry.
+// Precise boxes (matched only, chosen per chunk, CTA-uniform): every voxel
+// holds an int2 (hi, lo): hi sums the taps rounded to the CTA's unit
+// (scale = fx_budget / max tap), lo sums their exact rounding residuals
+// times lo_scale = 2^k (|residual| <= 1/2, so k is sized to keep the
+// per-voxel residual sum below 2^31).  value = (hi + lo / 2^k) / scale.
+// Used where a voxel's whole coverage can consist of tiny weights: the
+// int32 box resolves a tap only to 2.5e-7 of the CTA's largest tap, and
+// OS-SART's V = 1 / A^T 1 (algorithms.py:254-258) turns that into a
+// relative error of the update.  Also used everywhere when the int32
+// budget falls below the magic-add cap (pixels much finer than voxels:
+// many rays per voxel), where the residual word restores the resolution
+// the coarse unit gives up.
 //
 // MINB = CTAs per SM: 3 (72 registers, 72 KB boxes) or 4 (64 registers, 54 KB
 // boxes; 4 x 54 KB + the static arrays fit an SM's 228 KB), chosen per launch
 // by the slab size (launch_staged).
-template <int OP, int M, int MODE, bool WIDE = false, int MINB = 3>
+template <int OP, int M, int MODE, int MINB = 3>
 __global__ void __launch_bounds__(ST_THREADS, MINB)
     staged_kernel(const float* __restrict__ vol_in, float* __restrict__ vol_acc,
                   const AngleGeom* __restrict__ geom,
@@ -81,34 +91,32 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
                   int z_lo, int z_hi, int n_u, int n_v, int v_base, int v_end,
                   float* __restrict__ out, const float* __restrict__ proj_in,
                   const float* __restrict__ rb, const float* __restrict__ rw,
-                  int box_cap, float fx_budget, int vec_ok, int lane_stride) {
+                  int box_cap, float fx_budget, int vec_ok, int lane_stride,
+                  int prec_mode, float prec_fp, int edge, float lo_scale) {
   constexpr int T = 1 - M;
-  using Acc = typename std::conditional<WIDE, long long, int>::type;
   extern __shared__ float4 st_box4[];
   float* st_box = reinterpret_cast<float*>(st_box4);
-  Acc* box_i = reinterpret_cast<Acc*>(st_box4);
-  box_cap = WIDE ? box_cap / 2 : box_cap;  // in accumulator entries
-  // WIDE entries are two int32 words: the low 11 bits of every tap
-  // (0..2047) and the rest (v >> 11), each summed with a native ATOMS.ADD
-  // (sm_100 has no native 64-bit shared add: a CAS loop under contention
-  // was 8-20x slower); value = hi * 2048 + lo, exact for < 2^19 taps.
-  auto deposit = [](Acc* a, int v) {
-    if (WIDE) {
-      int* w = reinterpret_cast<int*>(a);
-      atomicAdd(w, v & 0x7FF);
-      atomicAdd(w + 1, v >> 11);
-    } else {
-      atomicAdd(reinterpret_cast<int*>(a), v);
-    }
+  int* box_i = reinterpret_cast<int*>(st_box4);
+  // one-word deposit (native ATOMS.ADD; sm_100 has no native fp32 or 64-bit
+  // shared add -- both compile to ATOMS.CAST.SPIN loops)
+  auto deposit = [&](int idx, float y, float w) {
+    atomicAdd(box_i + idx, magic_int(fmaf(y, w, ST_MAGIC)));
   };
-  auto widen = [](Acc raw) -> long long {
-    if (!WIDE) return (long long)raw;
-    const int2 w = *reinterpret_cast<const int2*>(&raw);
-    return (long long)w.y * 2048 + (long long)w.x;
+  // two-word deposit: rounded tap + exact residual (precise boxes)
+  auto deposit2 = [&](int idx, float y, float w) {
+    const float tb = fmaf(y, w, ST_MAGIC);
+    const float hf = tb - ST_MAGIC;   // round(y w), exact for |y w| < 2^22
+    const float e = fmaf(y, w, -hf);  // y w - round(y w), |e| <= 1/2
+    int* p = box_i + 2 * idx;
+    atomicAdd(p, magic_int(tb));
+    atomicAdd(p + 1, magic_int(fmaf(e, lo_scale, ST_MAGIC)));
   };
   __shared__ int ext[8];   // mlo, mhi, -, -, -, -, dir flags
   __shared__ int ext8[8];  // per chunk candidate: tlo, thi, zlo, zhi (x2)
   __shared__ float s_scale;
+  __shared__ float s_gap;  // largest neighbouring-ray slope difference
+  __shared__ float s_sqm;  // the source's q coordinate along M
+  __shared__ int s_pall;   // all chunks precise
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // lane_stride s (power of two <= ST_TV): the CTA covers 32 s columns x
@@ -148,6 +156,8 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
     ext[6] = 0;  // any ray marching -M
     ext[7] = 0;  // any ray marching +M
     s_scale = 0.f;
+    s_gap = 0.f;
+    s_sqm = 0.f;
   }
   __syncthreads();
   if (has) {
@@ -160,10 +170,38 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
     // per-CTA fixed-point scale: taps are |val| * step * w, w <= 1
     const float mag = has ? fabsf(val) * (float)r.step : 0.f;
     float wmax = mag;
-    for (int o = 16; o > 0; o >>= 1)
+    // Ray spacing for the precise-box rule: in voxel coordinates a ray is
+    // q_T = sq_T + s_T (q_M - sq_M) (sq = the source), so the rays of
+    // neighbouring pixels (u + 1, v + 1) sit |delta s| |q_M - sq_M| apart on
+    // plane q_M.  gap = the largest such slope difference (T or z).
+    float gap = 0.f;
+    if (has && prec_mode == 0 && prec_fp < 1e29f) {
+      const AngleGeom& ag = geom[a];
+      float P[3], Pu[3], Pv[3];
+#pragma unroll
+      for (int i = 0; i < 3; i++) {
+        const float iv = 1.f / (float)G.vox[i];
+        const float pi = (float)(ag.det00[i] + (double)u * ag.ustep[i] +
+                                 (double)v * ag.vstep[i] - ag.src[i]);
+        P[i] = pi * iv;
+        Pu[i] = (pi + (float)ag.ustep[i]) * iv;
+        Pv[i] = (pi + (float)ag.vstep[i]) * iv;
+      }
+      const float i0 = 1.f / P[M], iu = 1.f / Pu[M], iv = 1.f / Pv[M];
+      gap = fmaxf(fmaxf(fabsf(P[T] * i0 - Pu[T] * iu),
+                        fabsf(P[2] * i0 - Pu[2] * iu)),
+                  fmaxf(fabsf(P[T] * i0 - Pv[T] * iv),
+                        fabsf(P[2] * i0 - Pv[2] * iv)));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
       wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
-    if (lane == 0) atomicMax(reinterpret_cast<int*>(&s_scale),
-                             __float_as_int(wmax));  // non-negative floats
+      gap = fmaxf(gap, __shfl_xor_sync(0xffffffffu, gap, o));
+    }
+    if (lane == 0) {
+      atomicMax(reinterpret_cast<int*>(&s_scale),
+                __float_as_int(wmax));  // non-negative floats
+      atomicMax(reinterpret_cast<int*>(&s_gap), __float_as_int(gap));
+    }
   }
   __syncthreads();
   const int mlo = ext[0], mhi = ext[1];
@@ -185,6 +223,25 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
     inv_scale = fscale > 0.f ? 1.f / fscale : 0.f;
   }
   const float sv = OP == OP_BWD ? val * (float)r.step * fscale : 0.f;
+  // precise boxes: always (prec_mode 1), never (2), or (0) for CTAs whose
+  // tile lies within `edge` pixels of the detector border (voxels just
+  // outside the outermost rays see only their weight tails) and for chunks
+  // where neighbouring rays are >= prec_fp voxels apart (voxels between
+  // them likewise); CTA-uniform
+  // (kept in shared memory: read once per chunk, no registers held)
+  if (OP == OP_BWD && threadIdx.x == 0) {
+    bool pc = prec_mode == 1;
+    if (prec_mode == 0) {
+      const int tu = ST_TU * lane_stride, tv = ST_TV / lane_stride;
+      const int u_first = blockIdx.x * tu, v_first = v_base + blockIdx.y * tv;
+      pc = u_first < edge || u_first + tu > n_u - edge ||
+           v_first < edge || v_first + tv > n_v - edge;
+      const AngleGeom& ag = geom[a];
+      s_sqm = (float)((ag.src[M] - G.g0[M]) / G.vox[M] - 0.5);
+    }
+    s_pall = pc;  // every chunk precise
+    if (prec_mode == 2) s_gap = 0.f;
+  }
 
   float acc = 0.f;
   if (mixed) {
@@ -282,7 +339,16 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
       const int nby = M == 0 ? nt : S + 1;
       return M == 1 ? nbx * nby * nzz : nbx * (nby | 1) * nzz;
     };
-    const int ci = (ext8[0] > ext8[1] || box_size(0, ST_S) <= box_cap) ? 0 : 1;
+    bool prec = false;
+    if (OP == OP_BWD) {
+      const float c0f = (float)(dir > 0 ? cur : cur - ST_S + 1);
+      const float sq_m = s_sqm;
+      prec = s_pall ||
+             s_gap * fmaxf(fabsf(c0f - sq_m), fabsf(c0f + ST_S - sq_m)) >=
+                 prec_fp;
+    }
+    const int cap_eff = prec ? box_cap / 2 : box_cap;  // int2 entries
+    const int ci = (ext8[0] > ext8[1] || box_size(0, ST_S) <= cap_eff) ? 0 : 1;
     const int S = ST_S >> ci;
     const int c_lo = dir > 0 ? cur : cur - S + 1;
     cur += dir * S;
@@ -312,7 +378,7 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
     const int sy = M == 1 ? bn[0] : 1;
     const int sz = M == 1 ? bn[0] * bn[1] : bn[0] * sx;
     const int bsize = sz * bn[2];
-    const bool fits = !mixed && bsize <= box_cap;
+    const bool fits = !mixed && bsize <= cap_eff;
     const int qpr = bn[0] >> 2;            // x-quads per (y, z) row
     const int nquads = qpr * bn[1] * bn[2];
     const float inv_q = 1.f / (float)qpr, inv_y = 1.f / (float)bn[1];
@@ -372,17 +438,22 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
           }
         }
       } else {
-        for (int i = threadIdx.x; i < bsize; i += ST_THREADS) box_i[i] = 0;
+        const int nw = prec ? 2 * bsize : bsize;
+        for (int i = threadIdx.x; i < nw; i += ST_THREADS) box_i[i] = 0;
       }
       __syncthreads();
     }
-    // ---- samples of the chunk
-    if (any) {
+    // ---- samples of the chunk: one instantiation of the march per box
+    // mode (MODE_BOX: one-word box / Ax box reads, MODE_PREC: two-word
+    // box, MODE_GLOBAL: no box, straight from / to global memory), so the
+    // CTA-uniform mode is not re-tested per sample
+    auto march = [&](auto mode_tag) {
+      constexpr int BM = decltype(mode_tag)::value;
       // exact fixed-point positions (common.cuh), integer-advanced; on the
       // staged path relative to the box origin (an exact integer shift), so
       // the cells index the box directly
       long long qx = q_at(m, ka, 0), qy = q_at(m, ka, 1), qz = q_at(m, ka, 2);
-      if (fits) {
+      if (BM != 2) {
         qx -= (long long)bo[0] << QF;
         qy -= (long long)bo[1] << QF;
         qz -= (long long)bo[2] << QF;
@@ -391,7 +462,7 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
            kk++, qx += m.Bq[0], qy += m.Bq[1], qz += m.Bq[2]) {
         const float wx = q_frac(qx), wy = q_frac(qy), wz = q_frac(qz);
         const int ix = q_cell(qx), iy = q_cell(qy), iz = q_cell(qz);
-        if (fits) {
+        if (BM != 2) {
           const int b = iz * sz + iy * sy + ix * sx;
           if (OP == OP_FWD) {
             const float s000 = st_box[b], s001 = st_box[b + sx];
@@ -406,47 +477,30 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
             const float b0 = fmaf(wy, r01 - r00, r00);
             const float b1 = fmaf(wy, r11 - r10, r10);
             acc += fmaf(wz, b1 - b0, b0);
-          } else if (ST_PRECISE_W > 0.f &&
-                     fminf(fminf(fminf(wx, 1.f - wx), fminf(wy, 1.f - wy)),
-                           fminf(wz, 1.f - wz)) < ST_PRECISE_W) {
-            // a corner weight below ST_PRECISE_W: the box's fixed point
-            // (resolution 2.5e-7 of the CTA's largest tap) would cost such
-            // taps their relative accuracy, which voxels reached only by
-            // them (grid edges) need -- fp32 global atomics instead
-            const float t = val * (float)r.step;
-            const int ax = ix + bo[0], ay = iy + bo[1], az = iz + bo[2];
-#pragma unroll
-            for (int cz = 0; cz < 2; cz++) {
-              const int zi = az + cz;
-              if (zi < z_lo || zi >= z_hi) continue;
-              const float fz_ = cz ? wz : 1.f - wz;
-#pragma unroll
-              for (int cy = 0; cy < 2; cy++) {
-                const int yi = ay + cy;
-                if (yi < 0 || yi >= ny) continue;
-                const float fy_ = cy ? wy : 1.f - wy;
-#pragma unroll
-                for (int cx = 0; cx < 2; cx++) {
-                  const int xi = ax + cx;
-                  if (xi < 0 || xi >= nx) continue;
-                  atomicAdd(vol_acc + (size_t)(zi - z_lo) * plane +
-                                (size_t)yi * nx + xi,
-                            t * (fz_ * fy_ * (cx ? wx : 1.f - wx)));
-                }
-              }
-            }
           } else {
             const float z0 = sv * (1.f - wz), z1 = sv * wz;
             const float y00 = z0 * (1.f - wy), y01 = z0 * wy;
             const float y10 = z1 * (1.f - wy), y11 = z1 * wy;
-            deposit(&box_i[b], magic_int(fmaf(y00, 1.f - wx, ST_MAGIC)));
-            deposit(&box_i[b + sx], magic_int(fmaf(y00, wx, ST_MAGIC)));
-            deposit(&box_i[b + sy], magic_int(fmaf(y01, 1.f - wx, ST_MAGIC)));
-            deposit(&box_i[b + sy + sx], magic_int(fmaf(y01, wx, ST_MAGIC)));
-            deposit(&box_i[b + sz], magic_int(fmaf(y10, 1.f - wx, ST_MAGIC)));
-            deposit(&box_i[b + sz + sx], magic_int(fmaf(y10, wx, ST_MAGIC)));
-            deposit(&box_i[b + sz + sy], magic_int(fmaf(y11, 1.f - wx, ST_MAGIC)));
-            deposit(&box_i[b + sz + sy + sx], magic_int(fmaf(y11, wx, ST_MAGIC)));
+            const float vx = 1.f - wx;
+            if (BM == 1) {
+              deposit2(b, y00, vx);
+              deposit2(b + sx, y00, wx);
+              deposit2(b + sy, y01, vx);
+              deposit2(b + sy + sx, y01, wx);
+              deposit2(b + sz, y10, vx);
+              deposit2(b + sz + sx, y10, wx);
+              deposit2(b + sz + sy, y11, vx);
+              deposit2(b + sz + sy + sx, y11, wx);
+            } else {
+              deposit(b, y00, vx);
+              deposit(b + sx, y00, wx);
+              deposit(b + sy, y01, vx);
+              deposit(b + sy + sx, y01, wx);
+              deposit(b + sz, y10, vx);
+              deposit(b + sz + sx, y10, wx);
+              deposit(b + sz + sy, y11, vx);
+              deposit(b + sz + sy + sx, y11, wx);
+            }
           }
         } else {
           // overflow path: straight from / to global memory
@@ -476,6 +530,14 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
           }
         }
       }
+    };
+    if (any) {
+      if (!fits)
+        march(std::integral_constant<int, 2>());
+      else if (OP == OP_BWD && prec)
+        march(std::integral_constant<int, 1>());
+      else
+        march(std::integral_constant<int, 0>());
     }
     if (OP == OP_BWD && fits) {
       __syncthreads();
@@ -485,28 +547,43 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
       for (int qi = threadIdx.x; qi < nquads;
            qi += ST_THREADS, quad_next(xq, by, bz)) {
         const int d = bz * sz + by * sy + 4 * xq * sx;
-        Acc q0, q1, q2, q3;
-        if (M == 1 && !WIDE) {
-          const int4 q = *reinterpret_cast<const int4*>(box_i + d);
-          q0 = q.x; q1 = q.y; q2 = q.z; q3 = q.w;
+        float f0, f1, f2, f3;
+        if (prec) {
+          int2 q0, q1, q2, q3;
+          if (M == 1) {
+            const int4 a01 = *reinterpret_cast<const int4*>(box_i + 2 * d);
+            const int4 a23 = *reinterpret_cast<const int4*>(box_i + 2 * d + 4);
+            q0 = make_int2(a01.x, a01.y); q1 = make_int2(a01.z, a01.w);
+            q2 = make_int2(a23.x, a23.y); q3 = make_int2(a23.z, a23.w);
+          } else {
+            const int2* b2 = reinterpret_cast<const int2*>(box_i);
+            q0 = b2[d]; q1 = b2[d + sx]; q2 = b2[d + 2 * sx]; q3 = b2[d + 3 * sx];
+          }
+          if ((q0.x | q0.y | q1.x | q1.y | q2.x | q2.y | q3.x | q3.y) == 0)
+            continue;
+          const float il = inv_scale / lo_scale;
+          f0 = fmaf((float)q0.y, il, (float)q0.x * inv_scale);
+          f1 = fmaf((float)q1.y, il, (float)q1.x * inv_scale);
+          f2 = fmaf((float)q2.y, il, (float)q2.x * inv_scale);
+          f3 = fmaf((float)q3.y, il, (float)q3.x * inv_scale);
         } else {
-          q0 = box_i[d];
-          q1 = box_i[d + sx];
-          q2 = box_i[d + 2 * sx];
-          q3 = box_i[d + 3 * sx];
-        }
-        if ((q0 | q1 | q2 | q3) == 0) continue;
-        if (WIDE) {
-          q0 = widen(q0);
-          q1 = widen(q1);
-          q2 = widen(q2);
-          q3 = widen(q3);
+          int q0, q1, q2, q3;
+          if (M == 1) {
+            const int4 q = *reinterpret_cast<const int4*>(box_i + d);
+            q0 = q.x; q1 = q.y; q2 = q.z; q3 = q.w;
+          } else {
+            q0 = box_i[d];
+            q1 = box_i[d + sx];
+            q2 = box_i[d + 2 * sx];
+            q3 = box_i[d + 3 * sx];
+          }
+          if ((q0 | q1 | q2 | q3) == 0) continue;
+          f0 = (float)q0 * inv_scale; f1 = (float)q1 * inv_scale;
+          f2 = (float)q2 * inv_scale; f3 = (float)q3 * inv_scale;
         }
         const int gx = bo[0] + 4 * xq, gy = bo[1] + by, gz = bo[2] + bz;
         if (gy < 0 || gy >= ny || gz < z_lo || gz >= z_hi) continue;
         float* dst = vol_acc + (size_t)(gz - z_lo) * plane + (size_t)gy * nx;
-        const float f0 = (float)q0 * inv_scale, f1 = (float)q1 * inv_scale;
-        const float f2 = (float)q2 * inv_scale, f3 = (float)q3 * inv_scale;
         if (vec_ok && gx >= 0 && gx + 3 < nx) {
           st_red4(dst + gx, f0, f1, f2, f3);
         } else {
@@ -567,13 +644,14 @@ static double min_pixel_footprint(const double* grid6, int nx, int ny,
 // Returns the scale numerator: per CTA, scale = budget / max|val * step|.
 static float fixed_point_budget(const double* grid6, int nx, int ny, int nz,
                                 const double* geom, int n_a, int n_u, int n_v,
-                                double step_max) {
+                                double step_max, double* taps_bound = nullptr) {
   const double vmax = fmax(grid6[3], fmax(grid6[4], grid6[5]));
   double fp = min_pixel_footprint(grid6, nx, ny, nz, geom, n_a, n_u, n_v);
   fp = fmax(fp, 1e-3);
   const double rays = (2.0 / fp + 1.0) * (2.0 / fp + 1.0);
   const double samples = 2.0 * vmax / (0.5 * step_max) + 1.0;
   const double bound = fmin(rays, (double)ST_THREADS) * samples;
+  if (taps_bound) *taps_bound = bound;
   // per-voxel |sum| <= 2e9 < 2^31.  The bound counts every sample of a
   // ray in the 2x2x2 support at weight 1; the weights of one ray through
   // the support sum to at most 1 / step + 1 <= 4 / vmin + 1 voxels' worth
@@ -645,14 +723,38 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   // longer fits three)
   const size_t smem = (kb_knob ? (size_t)atoi(kb_knob) : four ? 54 : 72) * 1024;
   const int cap = (int)(smem / sizeof(float));
-  float budget =
+  double taps = 1.0;
+  const float budget =
       OP == OP_BWD ? fixed_point_budget(grid6, nx, ny, nz, geom, n_a, n_u, n_v,
-                                        step_max)
+                                        step_max, &taps)
                    : 0.f;
-  // int32 boxes while their budget reaches the magic-add cap (every
-  // production geometry so far); int64 boxes at the cap otherwise
-  const bool wide = OP == OP_BWD && budget < ST_BUDGET_CAP;
-  if (wide) budget = ST_BUDGET_CAP;
+  // Precise (two-word) boxes: everywhere when the int32 budget falls below
+  // the magic-add cap (many rays per voxel: the coarse unit gives up
+  // resolution that the residual word restores), else per chunk (the
+  // kernel's edge / ray-gap rule).  Knobs: CS_ST_PRECISE=0|1|auto,
+  // CS_ST_PRECISE_FP (ray gap in voxels; default 1.9 below 8 views).
+  static const char* pk = getenv("CS_ST_PRECISE");
+  static const char* pf = getenv("CS_ST_PRECISE_FP");
+  int prec_mode = 0;
+  if (pk && pk[0] == '1') prec_mode = 1;
+  if (pk && pk[0] == '0') prec_mode = 2;
+  if (OP == OP_BWD && budget < ST_BUDGET_CAP && prec_mode != 2) prec_mode = 1;
+  // the ray-gap rule (voxels between rays >= prec_fp voxels apart can get
+  // only tiny weights from every view) only matters when few views cover a
+  // voxel: on by default for launches of < 8 views (OS-SART blocks of a
+  // few views), any launch with the knob
+  const float prec_fp = pf ? (float)atof(pf) : (n_a < 8 ? 1.9f : 1e30f);
+  // residual scale 2^k: |residual| <= 1/2 per tap and at most `taps` taps
+  // per voxel and chunk, so the residual word stays below 2^30
+  int lo_k = 16;
+  while (lo_k > 0 && taps * ldexp(0.5, lo_k) >= 1073741824.0) lo_k--;
+  const float lo_scale = ldexpf(1.f, lo_k);
+  int edge = 0;
+  if (OP == OP_BWD) {
+    const double fp = min_pixel_footprint(grid6, nx, ny, nz, geom, n_a, n_u,
+                                          n_v);
+    edge = (int)fmin(ceil(1.0 / fmax(fp, 1e-3)) + 1.0, (double)max(n_u, n_v));
+  }
   const void* vbase = OP == OP_BWD ? (const void*)vol_acc : (const void*)vol_in;
   const int vec_ok = (nx % 4 == 0) && (((uintptr_t)vbase & 15) == 0);
   // v-band culling per main-axis class (runtime.cu slab_row_band); the
@@ -719,14 +821,8 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     const int rv = ST_TV / lane_stride;
     return (unsigned)((band[c][1] - band[c][0] + rv - 1) / rv);
   };
-  auto k0 = four ? (wide ? staged_kernel<OP, 0, MODE, true, 4>
-                         : staged_kernel<OP, 0, MODE, false, 4>)
-                  : (wide ? staged_kernel<OP, 0, MODE, true, 3>
-                          : staged_kernel<OP, 0, MODE, false, 3>);
-  auto k1 = four ? (wide ? staged_kernel<OP, 1, MODE, true, 4>
-                         : staged_kernel<OP, 1, MODE, false, 4>)
-                  : (wide ? staged_kernel<OP, 1, MODE, true, 3>
-                          : staged_kernel<OP, 1, MODE, false, 3>);
+  auto k0 = four ? staged_kernel<OP, 0, MODE, 4> : staged_kernel<OP, 0, MODE, 3>;
+  auto k1 = four ? staged_kernel<OP, 1, MODE, 4> : staged_kernel<OP, 1, MODE, 3>;
   // the dynamic shared-memory opt-in is per device: set it once on each
   // (the executor drives several GPUs from one process)
   static std::atomic<unsigned long long> attr_done{0};
@@ -734,14 +830,8 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   cudaGetDevice(&dev_ord);
   const unsigned long long bit = 1ull << (dev_ord & 63);
   if (!(attr_done.load() & bit)) {
-    for (auto k : {staged_kernel<OP, 0, MODE, false, 3>,
-                   staged_kernel<OP, 1, MODE, false, 3>,
-                   staged_kernel<OP, 0, MODE, true, 3>,
-                   staged_kernel<OP, 1, MODE, true, 3>,
-                   staged_kernel<OP, 0, MODE, false, 4>,
-                   staged_kernel<OP, 1, MODE, false, 4>,
-                   staged_kernel<OP, 0, MODE, true, 4>,
-                   staged_kernel<OP, 1, MODE, true, 4>})
+    for (auto k : {staged_kernel<OP, 0, MODE, 3>, staged_kernel<OP, 1, MODE, 3>,
+                   staged_kernel<OP, 0, MODE, 4>, staged_kernel<OP, 1, MODE, 4>})
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            200 * 1024);
     attr_done.fetch_or(bit);
@@ -750,14 +840,14 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     k0<<<dim3(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids, G, step_max, z_lo, z_hi, n_u, n_v,
         band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_ok,
-        lane_stride);
+        lane_stride, prec_mode, prec_fp, edge, lo_scale);
     CS_COUNT_LAUNCH();
   }
   if (nall > nxm && rows(1) > 0) {
     k1<<<dim3(gx, rows(1), nall - nxm), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids + nxm, G, step_max, z_lo, z_hi, n_u, n_v,
         band[1][0], band[1][1], out, proj_in, rb, rw, cap, budget, vec_ok,
-        lane_stride);
+        lane_stride, prec_mode, prec_fp, edge, lo_scale);
     CS_COUNT_LAUNCH();
   }
   e = cudaGetLastError();

@@ -91,6 +91,18 @@ __global__ void sart_update_kernel(float* __restrict__ x,
   }
 }
 
+__global__ void weighted_residual_kernel(float* __restrict__ r,
+                                         const float* __restrict__ b,
+                                         const float* __restrict__ w,
+                                         int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    const float d = b[i] - r[i];
+    r[i] = w ? w[i] * d : d;
+  }
+}
+
 __global__ void fill_kernel(float* __restrict__ x, float value, int64_t n) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -160,6 +172,16 @@ int cs_sart_update(float* x, float* upd, const float* v, double lam,
   if (n <= 0) return CS_OK;
   sart_update_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
       x, upd, v, (float)lam, n);
+  CS_COUNT_LAUNCH();
+  CS_CHECK_CUDA(cudaGetLastError());
+  return CS_OK;
+}
+
+int cs_weighted_residual(float* r, const float* b, const float* w, int64_t n,
+                         cs_stream_t stream) {
+  if (n <= 0) return CS_OK;
+  weighted_residual_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
+      r, b, w, n);
   CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   return CS_OK;

@@ -13,14 +13,16 @@ sm_100a kernels.
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 import torch
 import torch.distributed as dist
 
 from . import kernels as K
 
-__all__ = ["split_minimize_distributed", "exchange_halos", "gather_cores",
-           "CudaTvOps"]
+__all__ = ["split_minimize_distributed", "minimize_sharded", "exchange_halos",
+           "gather_cores", "CudaTvOps"]
 
 
 class CudaTvOps:
@@ -155,3 +157,92 @@ def split_minimize_distributed(u_full: torch.Tensor, slabs, params, rank: int,
     u = torch.empty_like(f)
     ops.rof_finish(f.contiguous(), p_full, u, params.lam)
     return u
+
+
+def _halo_fits(slabs) -> bool:
+    try:
+        _check_halo(slabs)
+    except ValueError:
+        return False
+    return all(t.core_range[1] > t.core_range[0] for t in slabs)
+
+
+def minimize_sharded(core: torch.Tensor, cores, params, rank: int,
+                     ops=CudaTvOps) -> torch.Tensor:
+    """split_minimize on a slab-sharded volume: rank r holds planes
+    ``cores[r]`` (``core``) and gets back its planes of the result -- the
+    full volume is never assembled.  Ghost planes come from the +-1
+    neighbours' cores (exchange_halos) when every halo fits inside the
+    neighbouring core; otherwise (halo deeper than a neighbour's slab) each
+    refresh all-gathers the cores and cuts the window from the full volume
+    (correct for any partition, at a volume's worth of traffic).  Matches
+    the single-process split_minimize on the same slab partition."""
+    from .regularization import HaloSlab, NormMode, TvMinimizer
+    d = params.effective_halo()
+    n_z = cores[-1][1]
+    slabs = [HaloSlab((z0, z1), d, (max(0, z0 - d), min(n_z, z1 + d)))
+             for z0, z1 in cores]
+    s = slabs[rank]
+    (z0, z1), (w0, w1) = s.core_range, s.window
+    c = s.core_in_window
+    plane_shape = tuple(core.shape[1:])
+    total = n_z * math.prod(plane_shape)
+    exchange = _halo_fits(slabs)
+
+    def refresh(w, zdim=0):
+        if exchange:
+            exchange_halos(w, slabs, rank, zdim)
+        else:
+            full = gather_cores(w, slabs, rank, None, zdim)
+            w.copy_(full.narrow(zdim, w0, w1 - w0))
+
+    if params.minimizer is TvMinimizer.GRADIENT_DESCENT:
+        w = torch.zeros((w1 - w0,) + plane_shape, dtype=torch.float32,
+                        device=core.device)
+        w[c].copy_(core)
+        spare = torch.empty_like(w)
+        ss = torch.zeros(1, dtype=torch.float64, device=w.device)
+        exact = params.norm_mode is NormMode.EXACT_GLOBAL
+        scale = 1.0 if exact else float(np.sqrt(total / max(1, w.numel())))
+        stored = hasattr(ops, "grad_store")
+        g = torch.empty_like(w) if stored else None
+        for _ in range(params.outer_syncs):
+            refresh(w)
+            for _ in range(params.inner_iters):
+                band = (c.start, c.stop) if exact else (0, w.shape[0])
+                if stored:
+                    ops.grad_store(w, g, band, ss)
+                else:
+                    ops.grad_sumsq(w, band, ss)
+                if exact:
+                    if ss.is_cuda and dist.get_backend() != "nccl":
+                        h = ss.cpu()
+                        dist.all_reduce(h)
+                        ss.copy_(h)
+                    else:
+                        dist.all_reduce(ss)
+                if stored:
+                    ops.step_g(w, g, spare, params.step, ss, scale)
+                else:
+                    ops.step(w, spare, params.step, ss, scale)
+                w, spare = spare, w
+        return w[c].contiguous()
+    # ROF: f's window is fixed; the dual p gets fresh ghosts every epoch and
+    # once more before the finish u = f + lam div p (div reads p at z - 1)
+    f = torch.zeros((w1 - w0,) + plane_shape, dtype=torch.float32,
+                    device=core.device)
+    f[c].copy_(core)
+    refresh(f)
+    p = torch.zeros((3, w1 - w0) + plane_shape, dtype=torch.float32,
+                    device=core.device)
+    q = torch.empty_like(p)
+    for epoch in range(params.outer_syncs):
+        if epoch > 0:
+            refresh(p, 1)
+        for _ in range(params.inner_iters):
+            ops.rof_iter(f, p, q, params.lam)
+            p, q = q, p
+    refresh(p, 1)
+    u = torch.empty_like(f)
+    ops.rof_finish(f, p, u, params.lam)
+    return u[c].contiguous()

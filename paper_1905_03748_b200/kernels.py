@@ -292,6 +292,14 @@ def sart_update(x, upd, v, lam: float, stream=None):
                                x.numel(), stream_ptr(stream)))
 
 
+def weighted_residual(r, b, w, stream=None):
+    """r = w * (b - r) elementwise (w None: r = b - r)."""
+    check(lib().cs_weighted_residual(dptr(r), dptr(b),
+                                     None if w is None else dptr(w),
+                                     r.numel(), stream_ptr(stream)))
+    return r
+
+
 def fill(x, value: float, stream=None):
     check(lib().cs_fill(dptr(x), float(value), x.numel(), stream_ptr(stream)))
     return x

@@ -221,3 +221,22 @@ def test_refine_for_overlap():
         assert flat[0] == 0 and flat[-1] == 25
         assert all(a[1] == b[0] for a, b in zip(out, out[1:]))
         assert all(b > a for a, b in out)
+
+
+def test_bench_self_launch_command():
+    """bench.py --gpus N (outside torchrun) starts N ranks through
+    torch.distributed.run on 127.0.0.1 with its own arguments."""
+    import importlib.util
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location(
+        "bench_mod", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    cmd = bench.launcher_cmd(["--gpus", "4", "--steps", "2"], 4, 29501)
+    assert cmd[:3] == [sys.executable, "-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--nnodes=1" in cmd
+    assert "--master-addr=127.0.0.1" in cmd and "--master-port=29501" in cmd
+    i = cmd.index(os.path.join(root, "bench.py"))
+    assert cmd[i + 1:] == ["--gpus", "4", "--steps", "2"]

@@ -25,6 +25,7 @@ FINE_FRACTION = float(os.environ.get("FUZZ_FINE", "0"))
 CLOSE = os.environ.get("FUZZ_CLOSE") == "1"
 MAX_VIEWS = int(os.environ.get("FUZZ_VIEWS", "12"))
 MAX_N = int(os.environ.get("FUZZ_MAXN", "40"))
+COARSE = os.environ.get("FUZZ_COARSE") == "1"
 
 
 def case(rng):
@@ -44,6 +45,10 @@ def case(rng):
     span = rng.uniform(0.6, 1.6) * (rng.uniform(0.05, 0.3) if fine else 1.0)
     pitch = (float(span * mag * max(ext[0], ext[1]) / nu),
              float(span * mag * ext[2] / nv))
+    if COARSE:  # large detectors of coarse pixels: rays 1.6-3 voxels apart
+        nu, nv = (int(v) for v in rng.integers(64, 129, 2))
+        fp = rng.uniform(1.6, 3.0, 2) * float(np.mean(vox))
+        pitch = (float(fp[0] * mag), float(fp[1] * mag))
     doff = (float(rng.uniform(-0.3, 0.3) * nu * pitch[0]),
             float(rng.uniform(-0.3, 0.3) * nv * pitch[1]))
     na = int(rng.integers(1, MAX_VIEWS + 1))
