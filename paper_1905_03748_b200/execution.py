@@ -571,11 +571,13 @@ def execute_forward(volume: Volume, geometry: ScanGeometry, pool: DevicePool,
     _run_devices(work, len(pool))
     rank, world = dist_info()
     if world > 1 and world == len(pool):
-        mine = parts[rank]
-        t = mine if isinstance(mine, torch.Tensor) else torch.from_numpy(mine)
-        dev = torch.device("cuda", torch.cuda.current_device())
-        full = _allgather_rows(t.to(dev), plan.angle_assignment, rank)
-        data = full if on_dev else full.cpu().numpy()
+        # every rank gets every rank's views, one bounded piece at a time,
+        # straight into the output (a device tensor only for device input)
+        shape = (n_angles, det.n_v, det.n_u)
+        data = (torch.empty(shape, dtype=torch.float32,
+                            device=volume.data.device) if on_dev
+                else np.empty(shape, np.float32))
+        _bcast_rows(data, parts[rank], plan.angle_assignment, rank)
     elif on_dev:
         data = torch.cat([torch.as_tensor(p).to(volume.data.device)
                           for p in parts if p is not None], 0)
@@ -752,11 +754,7 @@ def execute_backward(projections: ProjectionStack, geometry: ScanGeometry,
     _run_devices(work, D)
     rank, world = dist_info()
     if world > 1 and world == D:
-        full = _gather_slabs(res, slabs, queues, rank, res_dev)
-        if out is not None and not res_dev:
-            res[...] = full
-        else:
-            res = full
+        _gather_slabs(res, slabs, queues, rank, res_dev)
     _finish(devs, host_events, trace_sink)
     if out is not None:
         if isinstance(out.data, np.memmap):
@@ -766,17 +764,53 @@ def execute_backward(projections: ProjectionStack, geometry: ScanGeometry,
 
 
 def _gather_slabs(out, slabs, queues, rank, on_dev, device=None):
-    """Every rank ends with the full volume: broadcast each slab from its
-    owner (NCCL over NVLink between ranks; ``device`` is where host volumes
-    are staged for the collective, default the current GPU)."""
-    import torch.distributed as dist
-    if device is None:
-        device = torch.device("cuda", torch.cuda.current_device())
-    full = out if on_dev else torch.from_numpy(out).to(device)
+    """Every rank ends with the full volume: each slab is broadcast from
+    its owner in bounded pieces straight into ``out`` (host or device), so
+    no rank stages more than one piece beyond its output."""
     for owner, q in enumerate(queues):
         for si in q:
             z0, z1 = slabs[si]
-            part = full[z0:z1].contiguous()
-            dist.broadcast(part, src=owner)
-            full[z0:z1].copy_(part)
-    return full if on_dev else full.cpu().numpy()
+            _bcast_range(out, out[z0:z1] if owner == rank else None,
+                         (z0, z1), owner, rank, device)
+    return out
+
+
+PIECE_BYTES = 256 << 20
+
+
+def _bcast_range(out, mine, rng, owner, rank, device=None):
+    """out[r0:r1] = the owner's ``mine`` (rows r0..r1) on every rank, in
+    pieces of <= PIECE_BYTES.  NCCL broadcasts device buffers (NVLink);
+    gloo (tests) broadcasts host tensors."""
+    import torch.distributed as dist
+    r0, r1 = rng
+    if r1 <= r0:
+        return
+    row = int(np.prod(out.shape[1:])) * 4
+    step = max(1, PIECE_BYTES // max(1, row))
+    nccl = dist.get_backend() == "nccl"
+    if device is None and nccl:
+        device = torch.device("cuda", torch.cuda.current_device())
+    for p0 in range(r0, r1, step):
+        p1 = min(r1, p0 + step)
+        if owner == rank:
+            src = mine[p0 - r0:p1 - r0]
+            piece = (torch.as_tensor(src) if not isinstance(src, torch.Tensor)
+                     else src)
+            piece = piece.to(device if nccl else "cpu").contiguous()
+        else:
+            piece = torch.empty((p1 - p0,) + tuple(out.shape[1:]),
+                                dtype=torch.float32,
+                                device=device if nccl else "cpu")
+        dist.broadcast(piece, src=owner)
+        if isinstance(out, torch.Tensor):
+            out[p0:p1].copy_(piece)
+        else:
+            out[p0:p1] = piece.cpu().numpy()
+
+
+def _bcast_rows(out, mine, ranges, rank):
+    """Row-partitioned gather (ranges[r] owned by rank r; empty ranges and
+    missing parts allowed)."""
+    for owner, rng in enumerate(ranges):
+        _bcast_range(out, mine if owner == rank else None, rng, owner, rank)

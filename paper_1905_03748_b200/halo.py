@@ -72,7 +72,20 @@ def exchange_halos(w: torch.Tensor, slabs, rank: int, zdim: int = 0) -> None:
         if z1 > send_lo:
             ops.append(dist.P2POp(dist.isend,
                                   planes(send_lo, z1).contiguous(), rank + 1))
-    if ops:
+    if ops and w.is_cuda and dist.get_backend() != "nccl":
+        # gloo (ranks sharing a GPU in tests) moves host tensors only
+        staged = []
+        for op in ops:
+            h = op.tensor.cpu()
+            staged.append((op, h))
+        reqs = dist.batch_isend_irecv([dist.P2POp(op.op, h, op.peer)
+                                       for op, h in staged])
+        for req in reqs:
+            req.wait()
+        for op, h in staged:
+            if op.op is dist.irecv:
+                op.tensor.copy_(h)
+    elif ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
     for buf, (a, b) in keep:
@@ -90,8 +103,14 @@ def gather_cores(w: torch.Tensor, slabs, rank: int, full_shape,
     shape[zdim] = longest
     pad = torch.zeros(shape, dtype=w.dtype, device=w.device)
     pad.narrow(zdim, 0, z1 - z0).copy_(core)
-    parts = [torch.empty_like(pad) for _ in slabs]
-    dist.all_gather(parts, pad)
+    if pad.is_cuda and dist.get_backend() != "nccl":
+        hp = pad.cpu()
+        parts = [torch.empty_like(hp) for _ in slabs]
+        dist.all_gather(parts, hp)
+        parts = [p.to(pad.device) for p in parts]
+    else:
+        parts = [torch.empty_like(pad) for _ in slabs]
+        dist.all_gather(parts, pad)
     return torch.cat([p.narrow(zdim, 0, t.core_range[1] - t.core_range[0])
                       for p, t in zip(parts, slabs)], zdim)
 

@@ -203,22 +203,115 @@ def split_minimize(volume: Volume, pool: DevicePool, params: TvParams,
         raise ValueError("split minimization needs the full volume")
     n_slabs = _plan_slab_count(volume, pool, params, usable_fraction)
     slabs = make_halo_slabs(volume.grid.n_z, n_slabs, d)
+    if params.minimizer is TvMinimizer.GRADIENT_DESCENT and params.step <= 0:
+        raise ValueError("step must be positive")
+    if params.minimizer is TvMinimizer.ROF and params.lam <= 0:
+        raise ValueError("lambda must be positive")
     from .execution import dist_info
+    from . import halo
     rank, world = dist_info()
-    if world > 1 and world == len(slabs):
-        from . import halo
+    if world > 1 and world == len(slabs) and halo._halo_fits(slabs):
         u = halo.split_minimize_distributed(to_device(volume.data), slabs,
                                             params, rank)
         return _wrap(volume, u)
+    # all windows on one device when they fit beside the volume (GD: u, the
+    # snapshot, windows, spares, stored g ~ 5 volumes; ROF: f, p, snapshot
+    # ~ 7), else the windows stream through host memory one at a time
+    # (the reference's bound: one window plus its copies, :197-210)
+    grid = volume.grid
+    vol_bytes = grid.n_x * grid.n_y * (grid.n_z + 2 * d * len(slabs)) * 4
+    copies = 5 if params.minimizer is TvMinimizer.GRADIENT_DESCENT else 7
+    fits = copies * vol_bytes <= usable_fraction * pool.min_budget
+    if not volume.on_device and len(slabs) > 1 and not fits:
+        host = np.ascontiguousarray(to_host(volume.data), np.float32)
+        if params.minimizer is TvMinimizer.GRADIENT_DESCENT:
+            out = _split_gd_streamed(host, slabs, params)
+        else:
+            out = _split_rof_streamed(host, slabs, params)
+        return Volume(volume.grid, out, volume.slab_range)
     if params.minimizer is TvMinimizer.GRADIENT_DESCENT:
-        if params.step <= 0:
-            raise ValueError("step must be positive")
         u = _split_gd(to_device(volume.data), slabs, params)
     else:
-        if params.lam <= 0:
-            raise ValueError("lambda must be positive")
         u = _split_rof(to_device(volume.data), slabs, params)
     return _wrap(volume, u)
+
+
+def _h2d(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a)).to(
+        torch.device("cuda", torch.cuda.current_device()))
+
+
+def _split_gd_streamed(u: np.ndarray, slabs: list[HaloSlab],
+                       params: TvParams) -> np.ndarray:
+    """_split_gd with the windows kept in host memory and uploaded one at a
+    time (out-of-core volumes).  ExactGlobal couples the windows every inner
+    iteration, so each iteration is two passes: the window sums of g^2
+    (cs_tv_grad_sumsq), then the step with the total (cs_tv_step, which
+    recomputes g -- bit-identical to the stored-g pair); LocalApprox runs a
+    window's whole epoch on the device."""
+    u = u.copy()
+    total_voxels = u.size
+    exact = params.norm_mode is NormMode.EXACT_GLOBAL
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ss = torch.zeros(1, dtype=torch.float64, device=dev)
+    for _ in range(params.outer_syncs):
+        local = [u[s.window[0]:s.window[1]].copy() for s in slabs]
+        if exact:
+            for _ in range(params.inner_iters):
+                sums = torch.zeros(len(slabs), dtype=torch.float64,
+                                   device=dev)
+                for i, (s, w) in enumerate(zip(slabs, local)):
+                    c = s.core_in_window
+                    K.tv_grad_sumsq(_h2d(w), (c.start, c.stop),
+                                    sums[i:i + 1])
+                tot = sums.sum().reshape(1)
+                for i, w in enumerate(local):
+                    wd = _h2d(w)
+                    out = torch.empty_like(wd)
+                    K.tv_step(wd, out, params.step, tot, 1.0)
+                    local[i] = out.cpu().numpy()
+        else:
+            for i, w in enumerate(local):
+                wd = _h2d(w)
+                spare = torch.empty_like(wd)
+                g = torch.empty_like(wd)
+                scale = float(np.sqrt(total_voxels / wd.numel()))
+                for _ in range(params.inner_iters):
+                    K.tv_grad_store(wd, g, (0, wd.shape[0]), ss)
+                    K.tv_step_g(wd, g, spare, params.step, ss, scale)
+                    wd, spare = spare, wd
+                local[i] = wd.cpu().numpy()
+        for s, w in zip(slabs, local):
+            u[s.core_range[0]:s.core_range[1]] = w[s.core_in_window]
+    return u
+
+
+def _split_rof_streamed(f: np.ndarray, slabs: list[HaloSlab],
+                        params: TvParams) -> np.ndarray:
+    """_split_rof with f and the dual p in host memory, one window on the
+    device at a time; the finish u = f + lam div p per core with one ghost
+    plane on each side (div reads p at z - 1, and a window's last plane
+    would take the volume-face formula)."""
+    nz = f.shape[0]
+    p = np.zeros((3,) + f.shape, np.float32)
+    for _ in range(params.outer_syncs):
+        snap = p.copy()
+        for s in slabs:
+            w0, w1 = s.window
+            pl = _h2d(snap[:, w0:w1])
+            pl = _rof_iterations(_h2d(f[w0:w1]), pl, params.inner_iters,
+                                 params.lam)
+            z0, z1 = s.core_range
+            p[:, z0:z1] = pl[:, s.core_in_window].cpu().numpy()
+    u = np.empty_like(f)
+    for s in slabs:
+        z0, z1 = s.core_range
+        a, b = max(0, z0 - 1), min(nz, z1 + 1)
+        fd = _h2d(f[a:b])
+        ud = torch.empty_like(fd)
+        K.rof_finish(fd, _h2d(p[:, a:b]), ud, params.lam)
+        u[z0:z1] = ud[z0 - a:z1 - a].cpu().numpy()
+    return u
 
 
 def _split_gd(u0: torch.Tensor, slabs: list[HaloSlab],

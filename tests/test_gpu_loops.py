@@ -222,13 +222,17 @@ def test_distributed_loops_on_gpu_vs_oracle(world):
     port = s.getsockname()[1]
     s.close()
     ctx = mp.get_context("spawn")
-    q = ctx.SimpleQueue()
+    q = ctx.Queue()
     procs = [ctx.Process(target=_dist_loop_worker, args=(r, world, port, q))
              for r in range(world)]
     for p in procs:
         p.start()
-    errs = q.get()
-    for p in procs:
-        p.join(timeout=300)
-        assert p.exitcode == 0
+    try:
+        errs = q.get(timeout=600)
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    assert all(p.exitcode == 0 for p in procs)
     assert max(errs.values()) <= TOL_LOOP, errs
