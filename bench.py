@@ -657,21 +657,31 @@ def run_extras(args, cs, K, g, vol, y, dev):
     out["atb_matched_sparse_gups"] = upd / rate(
         lambda: K.bwd_matched(sparse, g, (0, A), (0, n), acc), 1) / 1e9
     del sparse
-    # TV-GD iteration as the loops run it (g + Sigma g^2 pass, streaming
-    # step pass) and ROF dual iteration on the 512^3 volume (SURVEY 8(d):
-    # 12 / 28 B per voxel-iteration algorithmic)
+    # TV-GD iteration as the loops run it: in steady state one fused pass
+    # per iteration (step i + gradient i+1 + Sigma g^2, tv.cu
+    # tv_march_kernel); "tv_gd_run" times a whole 10-iteration
+    # minimize_tv_gradient (gradient pass, 9 fused passes, final step, the
+    # input copy).  ROF: one dual iteration.  512^3 volume; 12 /
+    # 28 B per voxel-iteration algorithmic.
+    from paper_1905_03748_b200 import regularization as REG
     u2 = torch.empty_like(vol)
     g2 = torch.empty_like(vol)
+    g3 = torch.empty_like(vol)
     ss = torch.zeros(1, dtype=torch.float64, device=dev)
+    ss2 = torch.zeros_like(ss)
+    K.tv_grad_store(vol, g2, (0, n), ss)
     p3 = torch.zeros((3,) + tuple(vol.shape), device=dev)
     q3 = torch.empty_like(p3)
-    for name, fn, bpv in (
-            ("tv_gd", lambda: (K.tv_grad_store(vol, g2, (0, n), ss),
-                               K.tv_step_g(vol, g2, u2, 1e-3, ss, 1.0)), 12.0),
-            ("tv_rof", lambda: K.rof_iter(vol, p3, q3, 0.1), 28.0)):
-        t = rate(fn, 5)
+    for name, fn, bpv, its in (
+            ("tv_gd", lambda: K.tv_gd_fused(vol, g2, u2, g3, (0, n), 1e-3,
+                                            ss, 1.0, ss2), 12.0, 1),
+            ("tv_gd_run", lambda: REG._gd_iterations(vol, 10, 1e-3), 12.0,
+             10),
+            ("tv_rof", lambda: K.rof_iter(vol, p3, q3, 0.1), 28.0, 1)):
+        t = rate(fn, 5) / its
         out[f"{name}_gvox_iter_per_s"] = vol.numel() / t / 1e9
         out[f"{name}_hbm_frac"] = vol.numel() * bpv / t / (peak * 1e9)
+    del u2, g3, ss2
     del u2, g2, p3, q3, acc
 
     # end-to-end through the public API with pinned host buffers:

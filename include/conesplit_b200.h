@@ -149,6 +149,18 @@ int cs_tv_grad_store(const float* u, float* g, int nx, int ny, int nzw,
 int cs_tv_step_g(const float* u, const float* g, float* u_out, int64_t n,
                  double step, const double* norm_sumsq_dev, double scale,
                  cs_stream_t stream);
+/* One whole GD iteration after the first, in ONE pass (replaces the
+ * reference's loop body regularization.py:145-150 for iterations >= 2):
+ *   u_out = u - step * g / (sqrt(*norm_sumsq_dev) * scale)   (every voxel)
+ *   g_out = TV subgradient of u_out over the window, *out_sum = sum of
+ *           g_out^2 over the core planes [core_lo, core_hi)
+ * u_out / g_out are bit-identical to cs_tv_step_g followed by
+ * cs_tv_grad_store.  norm_sumsq_dev and out_sum must differ (the kernel reads
+ * one while the reduction writes the other). */
+int cs_tv_gd_fused(const float* u, const float* g, float* u_out, float* g_out,
+                   int nx, int ny, int nzw, int core_lo, int core_hi,
+                   double step, const double* norm_sumsq_dev, double scale,
+                   double* out_sum, cs_stream_t stream);
 
 /* One Chambolle dual iteration (regularization.py:174-182):
  *   u = f + lam div p; p += (1/12/lam) ∇u; p /= max(1, |p|)

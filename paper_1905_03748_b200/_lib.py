@@ -54,6 +54,7 @@ SYMBOLS: dict[str, list] = {
     "cs_tv_grad_norm": [P, I, I, I, I, I, P, P],
     "cs_tv_grad_store": [P, P, I, I, I, I, I, P, P],
     "cs_tv_step_g": [P, P, P, L, D, P, D, P],
+    "cs_tv_gd_fused": [P, P, P, P, I, I, I, I, I, D, P, D, P, P],
     "cs_tv_step": [P, P, I, I, I, D, P, D, P],
     "cs_rof_iter": [P, P, P, I, I, I, D, P],
     "cs_rof_finish": [P, P, P, I, I, I, D, P],

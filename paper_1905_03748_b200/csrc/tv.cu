@@ -72,7 +72,18 @@ __global__ void __launch_bounds__(256)
             blockIdx.x] = s;
 }
 
-// ---- tiled TV-GD (production) ---------------------------------------------
+// 1 / sqrt(gx^2 + gy^2 + gz^2 + eps) with the rounding order pinned (no
+// contraction freedom), so every GD kernel produces the same bits; the
+// argument is >= eps (normal), where the ftz approximation equals rsqrtf.
+__device__ __forceinline__ float tv_inv_norm(float gx, float gy, float gz) {
+  const float n = __fadd_rn(
+      __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, __fmul_rn(gx, gx))), (float)TV_EPS);
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(n));
+  return r;
+}
+
+// ---- tiled TV-GD (r01; A/B baseline and the two-pass norm/step pair) ---------------------------------------------
 // CTA = 32 x 8 (x, y) tile marching over a chunk of TV_ZC planes.  Per plane
 // the normalised gradient p is computed ONCE per voxel (plus a one-voxel
 // halo at x - 1 / y - 1) from two rotating u-planes in shared memory; pz of
@@ -185,8 +196,7 @@ __global__ void __launch_bounds__(TV_TX * TV_TY)
         const float gxv = (f & 2u) ? pl0[k + 1] - cc : 0.f;
         const float gyv = (f & 4u) ? pl0[k + TV_UX] - cc : 0.f;
         const float gzv = zlast ? 0.f : pl1[k] - cc;
-        const float inv =
-            rsqrtf(gxv * gxv + gyv * gyv + gzv * gzv + (float)TV_EPS);
+        const float inv = tv_inv_norm(gxv, gyv, gzv);
         px = gxv * inv;
         py = gyv * inv;
         pz = gzv * inv;
@@ -229,6 +239,166 @@ __global__ void __launch_bounds__(TV_TX * TV_TY)
       partial[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x +
               blockIdx.x] = sm;
     }
+  }
+}
+
+// ---- marching TV-GD (production) ----------------------------------------
+// One pass per iteration.  Iteration i of GD is u_{i+1} = u_i - c_i g_i with
+// c_i = step / ||g_i|| (regularization.py:145-150), and g_{i+1} = grad TV
+// (u_{i+1}).  The norm is global, so u_{i+1} cannot be written before g_i is
+// complete -- but g_{i+1} can be computed in the same pass that applies the
+// step: every thread forms u_{i+1} = u_i - c_i g_i on the fly from the u_i,
+// g_i it loads, and the stencil runs on those values.  The pass reads u_i,
+// g_i and writes u_{i+1}, g_{i+1} (16 B / voxel) plus the partial sums of
+// g_{i+1}^2; the first iteration reads u only (tv_march<0>, = grad_store)
+// and the last applies its step with the float4 stream (tv_step_g_kernel).
+//
+// CTA = 16 warps; lane l <-> x = x0 - 1 + l, warp w <-> y = y0 - 1 + w.
+// Lane 0 / warp 0 are a one-voxel halo whose p feeds the divergence; lane 31
+// / warp 15 only supply u(x+1) / u(y+1) to their neighbours: 30 x 14 outputs
+// per CTA, and no thread loads anything but its own voxel.  Each thread
+// marches its column in z over a chunk of TM_ZC planes: u(x+1) by
+// shfl_down, p(x-1) by shfl_up, u(y+1) and p(y-1) through two double-buffered
+// shared rows (one barrier per plane), pz(z-1) in a register.  Loads run
+// TM_D planes ahead through a per-thread cp.async ring (zero-fill outside the
+// window); a thread reads back only its own slots, so the ring needs no
+// barrier.  Same per-voxel expressions as tv_gd_tiled_kernel and the step of
+// tv_step_g_kernel (fp64 u - c g), so g and u are bit-identical to
+// grad_store + step_g; only the grouping of the fp64 partial sums differs.
+constexpr int TM_WARPS = 16, TM_THREADS = 32 * TM_WARPS;
+constexpr int TM_OX = 30, TM_OY = TM_WARPS - 2;
+#ifndef CS_TM_ZC
+#define CS_TM_ZC 32
+#endif
+constexpr int TM_ZC = CS_TM_ZC;
+constexpr int TM_NS = 8;         // ring stages (power of two)
+constexpr int TM_D = TM_NS - 1;  // planes in flight
+
+__device__ __forceinline__ void cp_async4(unsigned dst, const float* src,
+                                          bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst),
+               "l"(src), "r"(ok ? 4 : 0)  // 0: zero-fill, nothing read
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// FUSED 0: g = grad TV(u) -> gout (window), sum g^2 over the core.
+// FUSED 1: u' = u - c g (c from sumsq_in) -> uo, g' = grad TV(u') -> gout.
+template <int FUSED>
+__global__ void __launch_bounds__(TM_THREADS, 2)
+    tv_march_kernel(const float* __restrict__ u, const float* __restrict__ gin,
+                    float* __restrict__ uo, float* __restrict__ gout, Win W,
+                    int c_lo, int c_hi, double step,
+                    const double* __restrict__ sumsq_in, double scale,
+                    double* __restrict__ partial) {
+  constexpr int NA = FUSED ? 2 : 1;  // arrays loaded per voxel
+  __shared__ float ring[TM_NS][NA][TM_THREADS];
+  __shared__ float su[2][TM_WARPS][32];   // u rows (for gy)
+  __shared__ float spy[2][TM_WARPS][32];  // py rows (for div)
+  __shared__ double sred[TM_WARPS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tid = threadIdx.x;
+  const int x = blockIdx.x * TM_OX - 1 + lane;
+  const int y = blockIdx.y * TM_OY - 1 + w;
+  const int zb = blockIdx.z * TM_ZC;
+  const int ze = min(W.nz, zb + TM_ZC);
+  const bool in_xy = x >= 0 && x < W.nx && y >= 0 && y < W.ny;
+  const bool own = in_xy && lane > 0 && lane < 31 && w > 0 && w < TM_WARPS - 1;
+  const bool xl = x < W.nx - 1, yl = y < W.ny - 1;  // forward diffs exist
+  const size_t plane = (size_t)W.nx * W.ny;
+  const int off = in_xy ? y * W.nx + x : 0;
+  double coef = 0.0;
+  if (FUSED) {
+    const double norm = sqrt(*sumsq_in) * scale;
+    coef = norm < 1e-30 ? 0.0 : step / norm;  // regularization.py:148-149
+  }
+  // ring slot of this thread, stage 0 / array 0; stage stride, array stride
+  const unsigned ring0 = (unsigned)__cvta_generic_to_shared(&ring[0][0][tid]);
+  constexpr unsigned RS = NA * TM_THREADS * 4, RA = TM_THREADS * 4;
+  // issue pointer: plane zi of the next load
+  int zi = zb - 1;
+  const float* pu = u + (ptrdiff_t)zi * (ptrdiff_t)plane + off;
+  const float* pg = FUSED ? gin + (ptrdiff_t)zi * (ptrdiff_t)plane + off : u;
+  auto issue = [&]() {
+    const bool ok = in_xy && (unsigned)zi < (unsigned)W.nz;
+    const unsigned st = ring0 + ((zi - zb + 1) & (TM_NS - 1)) * RS;
+    cp_async4(st, ok ? pu : u, ok);
+    if (FUSED) cp_async4(st + RA, ok ? pg : u, ok);
+    cp_async_commit();
+    zi++;
+    pu += plane;
+    if (FUSED) pg += plane;
+  };
+  auto take = [&](int zz) {
+    const int st = (zz - zb + 1) & (TM_NS - 1);
+    const float uu = ring[st][0][tid];
+    if (!FUSED) return uu;
+    const float gg = ring[st][NA - 1][tid];
+    return (float)((double)uu - coef * (double)gg);  // as tv_step_g_kernel
+  };
+#pragma unroll
+  for (int i = 0; i <= TM_D - 1; i++) issue();  // planes zb-1 .. zb-2+D
+  cp_async_wait<TM_D - 1>();
+  float uc = take(zb - 1);
+  su[(zb - 1) & 1][w][lane] = uc;
+  __syncthreads();
+  float pz_prev = 0.f;
+  double acc = 0.0;
+  float* po = gout + (ptrdiff_t)zb * (ptrdiff_t)plane + off;
+  float* puo = FUSED ? uo + (ptrdiff_t)zb * (ptrdiff_t)plane + off : nullptr;
+  const int wy = w < TM_WARPS - 1 ? w + 1 : w;
+  // branch-free masks: p = 0 outside the window (all three differences
+  // masked) and each forward difference zero where it is undefined
+  const float mx = (in_xy && xl) ? 1.f : 0.f;
+  const float my = (in_xy && yl) ? 1.f : 0.f;
+  const int zlo_sum = max(zb, c_lo), zhi_sum = own ? c_hi : INT_MIN;
+  for (int z = zb - 1; z < ze; z++) {
+    issue();                    // plane z + D
+    cp_async_wait<TM_D - 1>();  // plane z + 1 landed (own slots only)
+    const float un = take(z + 1);
+    // p(z) at (x, y): forward differences, zero on the undefined faces
+    const float ux = __shfl_down_sync(0xffffffffu, uc, 1);
+    const float uy = su[z & 1][wy][lane];
+    const float mz = (in_xy && z >= 0 && z < W.nz - 1) ? 1.f : 0.f;
+    const float gxv = (ux - uc) * mx;
+    const float gyv = (uy - uc) * my;
+    const float gzv = (un - uc) * mz;
+    const float inv = tv_inv_norm(gxv, gyv, gzv);
+    const float px = gxv * inv, py = gyv * inv;
+    const float pz = (in_xy && z >= 0) ? gzv * inv : 0.f;
+    spy[z & 1][w][lane] = py;
+    su[(z + 1) & 1][w][lane] = un;
+    __syncthreads();
+    const float pxm = __shfl_up_sync(0xffffffffu, px, 1);
+    const float pym = spy[z & 1][w > 0 ? w - 1 : 0][lane];
+    const float g = -((pz - pz_prev) + (py - pym) + (px - pxm));
+    if (z >= zb) {
+      if (own) {
+        *po = g;
+        if (FUSED) *puo = uc;
+      }
+      po += plane;
+      if (FUSED) puo += plane;
+    }
+    const float gs = (z >= zlo_sum && z < zhi_sum) ? g : 0.f;
+    acc += (double)gs * (double)gs;
+    pz_prev = pz;
+    uc = un;
+  }
+  cp_async_wait<0>();
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) sred[w] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double sm = 0.0;
+    for (int i = 0; i < TM_WARPS; i++) sm += sred[i];
+    partial[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x +
+            blockIdx.x] = sm;
   }
 }
 
@@ -463,15 +633,62 @@ int cs_tv_grad_store(const float* u, float* g, int nx, int ny, int nzw,
              "bad core [%d, %d) in window of %d", core_lo, core_hi, nzw);
   CS_REQUIRE(u != g, CS_ERR_ARG, "cs_tv_grad_store: g aliases u");
   cudaStream_t s = (cudaStream_t)stream;
-  const dim3 grid((nx + TV_TX - 1) / TV_TX, (ny + TV_TY - 1) / TV_TY,
-                  (nzw + TV_ZC - 1) / TV_ZC);
+  static const char* tiled = getenv("CS_TV_TILED");  // A/B: r01 kernel
+  if (tiled && tiled[0] == '1') {
+    const dim3 grid((nx + TV_TX - 1) / TV_TX, (ny + TV_TY - 1) / TV_TY,
+                    (nzw + TV_ZC - 1) / TV_ZC);
+    const size_t nb = (size_t)grid.x * grid.y * grid.z;
+    double* part = nullptr;
+    retain_pool();
+    CS_CHECK_CUDA(cudaMallocAsync((void**)&part, nb * sizeof(double), s));
+    tv_gd_tiled_kernel<2><<<grid, dim3(TV_TX, TV_TY), 0, s>>>(
+        u, g, Win{nx, ny, nzw}, 0, nzw, 0.0, nullptr, 1.0, part, core_lo,
+        core_hi);
+    CS_COUNT_LAUNCH();
+    CS_CHECK_CUDA(cudaGetLastError());
+    rc = reduce_into(part, nb, out_sum, s);
+    cudaFreeAsync(part, s);
+    return rc;
+  }
+  const dim3 grid((nx + TM_OX - 1) / TM_OX, (ny + TM_OY - 1) / TM_OY,
+                  (nzw + TM_ZC - 1) / TM_ZC);
   const size_t nb = (size_t)grid.x * grid.y * grid.z;
   double* part = nullptr;
   retain_pool();
   CS_CHECK_CUDA(cudaMallocAsync((void**)&part, nb * sizeof(double), s));
-  tv_gd_tiled_kernel<2><<<grid, dim3(TV_TX, TV_TY), 0, s>>>(
-      u, g, Win{nx, ny, nzw}, 0, nzw, 0.0, nullptr, 1.0, part, core_lo,
-      core_hi);
+  tv_march_kernel<0><<<grid, TM_THREADS, 0, s>>>(
+      u, nullptr, nullptr, g, Win{nx, ny, nzw}, core_lo, core_hi, 0.0,
+      nullptr, 1.0, part);
+  CS_COUNT_LAUNCH();
+  CS_CHECK_CUDA(cudaGetLastError());
+  rc = reduce_into(part, nb, out_sum, s);
+  cudaFreeAsync(part, s);
+  return rc;
+}
+
+int cs_tv_gd_fused(const float* u, const float* g, float* u_out, float* g_out,
+                   int nx, int ny, int nzw, int core_lo, int core_hi,
+                   double step, const double* norm_sumsq_dev, double scale,
+                   double* out_sum, cs_stream_t stream) {
+  int rc = check_win(nx, ny, nzw);
+  if (rc) return rc;
+  CS_REQUIRE(0 <= core_lo && core_lo < core_hi && core_hi <= nzw, CS_ERR_ARG,
+             "bad core [%d, %d) in window of %d", core_lo, core_hi, nzw);
+  CS_REQUIRE(u != u_out && u != g_out && g != u_out && g != g_out &&
+                 u_out != g_out,
+             CS_ERR_ARG, "cs_tv_gd_fused: outputs alias inputs or each other");
+  CS_REQUIRE(norm_sumsq_dev != out_sum, CS_ERR_ARG,
+             "cs_tv_gd_fused: the input and output sums must differ");
+  cudaStream_t s = (cudaStream_t)stream;
+  const dim3 grid((nx + TM_OX - 1) / TM_OX, (ny + TM_OY - 1) / TM_OY,
+                  (nzw + TM_ZC - 1) / TM_ZC);
+  const size_t nb = (size_t)grid.x * grid.y * grid.z;
+  double* part = nullptr;
+  retain_pool();
+  CS_CHECK_CUDA(cudaMallocAsync((void**)&part, nb * sizeof(double), s));
+  tv_march_kernel<1><<<grid, TM_THREADS, 0, s>>>(
+      u, g, u_out, g_out, Win{nx, ny, nzw}, core_lo, core_hi, step,
+      norm_sumsq_dev, scale, part);
   CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   rc = reduce_into(part, nb, out_sum, s);

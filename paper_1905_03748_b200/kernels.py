@@ -221,6 +221,21 @@ def tv_step_g(u: torch.Tensor, g: torch.Tensor, u_out: torch.Tensor,
     return u_out
 
 
+def tv_gd_fused(u: torch.Tensor, g: torch.Tensor, u_out: torch.Tensor,
+                g_out: torch.Tensor, core, step: float, sumsq: torch.Tensor,
+                scale: float, out: torch.Tensor, stream=None):
+    """One GD iteration after the first in one pass: u_out = u - step g /
+    (sqrt(sumsq) scale); g_out = TV subgradient of u_out; out[0] = Σg_out²
+    over the core planes (= tv_step_g then tv_grad_store, bit for bit)."""
+    nz, ny, nx = u.shape
+    check(lib().cs_tv_gd_fused(dptr(_f32(u, "u")), dptr(_f32(g, "g")),
+                               dptr(_f32(u_out, "u_out")),
+                               dptr(_f32(g_out, "g_out")), nx, ny, nz,
+                               core[0], core[1], float(step), dptr(sumsq),
+                               float(scale), dptr(out), stream_ptr(stream)))
+    return u_out
+
+
 def tv_grad_norm(u: torch.Tensor, core, out: torch.Tensor, stream=None):
     """out[0] = ||g||_2 over the core planes (regularization.py:147)."""
     nz, ny, nx = u.shape

@@ -123,15 +123,23 @@ def _gd_iterations(u: torch.Tensor, iters: int, step: float) -> torch.Tensor:
     """iters x { g = TV subgradient; u -= step g / ||g|| } on one window
     (faces at its ends), all on device."""
     nz = u.shape[0]
+    if iters <= 0:
+        return u.clone()
     a = u.clone()
     b = torch.empty_like(a)
-    g = torch.empty_like(a)  # g kept between the passes: the step streams
-    ss = _scalar(a.device)
-    for _ in range(iters):
-        K.tv_grad_store(a, g, (0, nz), ss)
-        K.tv_step_g(a, g, b, step, ss, 1.0)
+    g = torch.empty_like(a)  # g kept between the passes
+    g2 = torch.empty_like(a)
+    ss, ss2 = _scalar(a.device), _scalar(a.device)
+    # iteration 1's gradient, then one fused pass per further iteration
+    # (step i + gradient i+1, tv.cu tv_march_kernel), then the last step
+    K.tv_grad_store(a, g, (0, nz), ss)
+    for _ in range(iters - 1):
+        K.tv_gd_fused(a, g, b, g2, (0, nz), step, ss, 1.0, ss2)
         a, b = b, a
-    return a
+        g, g2 = g2, g
+        ss, ss2 = ss2, ss
+    K.tv_step_g(a, g, b, step, ss, 1.0)
+    return b
 
 
 def minimize_tv_gradient(volume: Volume, params: TvParams) -> Volume:
@@ -331,20 +339,38 @@ def _split_gd(u0: torch.Tensor, slabs: list[HaloSlab],
         local = [snap[s.window[0]:s.window[1]].clone() for s in slabs]
         spare = [torch.empty_like(w) for w in local]
         gs = [torch.empty_like(w) for w in local]
-        for _ in range(params.inner_iters):
-            for i, (s, w) in enumerate(zip(slabs, local)):
-                core = s.core_in_window if exact else slice(0, w.shape[0])
-                K.tv_grad_store(w, gs[i], (core.start, core.stop),
-                                sums[i:i + 1])
+        gs2 = [torch.empty_like(w) for w in local]
+        cores = [s.core_in_window if exact else slice(0, w.shape[0])
+                 for s, w in zip(slabs, local)]
+        scales = [1.0 if exact else float(np.sqrt(total_voxels / w.numel()))
+                  for w in local]
+        sums2 = torch.zeros_like(sums)
+
+        def norms():  # the sum each window's step divides by
             if exact:
                 tot = sums.sum().reshape(1)
+                return [tot] * len(local)
+            return [sums[i:i + 1] for i in range(len(local))]
+        if params.inner_iters > 0:
+            # first gradient, then one fused pass (step + next gradient)
+            # per further iteration, then the last step
+            for i, w in enumerate(local):
+                K.tv_grad_store(w, gs[i], (cores[i].start, cores[i].stop),
+                                sums[i:i + 1])
+            for _ in range(params.inner_iters - 1):
+                nrm = norms()
                 for i, w in enumerate(local):
-                    K.tv_step_g(w, gs[i], spare[i], params.step, tot, 1.0)
-            else:
-                for i, w in enumerate(local):
-                    scale = float(np.sqrt(total_voxels / w.numel()))
-                    K.tv_step_g(w, gs[i], spare[i], params.step,
-                                sums[i:i + 1], scale)
+                    K.tv_gd_fused(w, gs[i], spare[i], gs2[i],
+                                  (cores[i].start, cores[i].stop),
+                                  params.step, nrm[i], scales[i],
+                                  sums2[i:i + 1])
+                local, spare = spare, local
+                gs, gs2 = gs2, gs
+                sums, sums2 = sums2, sums
+            nrm = norms()
+            for i, w in enumerate(local):
+                K.tv_step_g(w, gs[i], spare[i], params.step, nrm[i],
+                            scales[i])
             local, spare = spare, local
         for s, w in zip(slabs, local):
             u[s.core_range[0]:s.core_range[1]] = w[s.core_in_window]

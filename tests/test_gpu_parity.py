@@ -730,10 +730,10 @@ def test_tv_grad_norm_and_sumsq_vs_oracle(golden):
 
 
 def test_tv_stored_g_pair_bit_identical():
-    """cs_tv_grad_store + cs_tv_step_g (the production GD iteration) give
-    exactly the bits of cs_tv_grad_sumsq + cs_tv_step over a whole window
-    (a core band: the same up to the grouping of the fp64 partial sums);
-    odd sizes exercise the scalar tail of the streaming step."""
+    """cs_tv_grad_store + cs_tv_step_g (the production GD pieces) agree with
+    cs_tv_grad_sumsq + cs_tv_step up to the grouping of the fp64 partial
+    sums (different kernels); odd sizes exercise the scalar tail of the
+    streaming step."""
     import torch
     from paper_1905_03748_b200 import kernels as K
     u = torch.rand((13, 11, 9), device="cuda")
@@ -747,12 +747,100 @@ def test_tv_stored_g_pair_bit_identical():
         K.tv_grad_store(u, g, core, s2)
         o2 = torch.empty_like(u)
         K.tv_step_g(u, g, o2, 0.05, s2, 1.3)
-        if core == (0, 13):
-            assert torch.equal(s1, s2)
-            assert torch.equal(o1, o2)
-        else:  # the core's fp64 partials are grouped differently
-            assert abs(float(s1) - float(s2)) <= 1e-12 * float(s1)
-            assert torch.allclose(o1, o2, rtol=1e-6, atol=1e-7)
+        # the two kernels group the fp64 partial sums differently (the
+        # per-voxel g^2 terms are the same bits)
+        assert abs(float(s1) - float(s2)) <= 1e-12 * float(s1)
+        assert torch.allclose(o1, o2, rtol=1e-6, atol=1e-7)
+
+
+def test_tv_gd_fused_bit_identical():
+    """cs_tv_gd_fused (step i + gradient i+1 in one pass) gives exactly the
+    bits of cs_tv_step_g followed by cs_tv_grad_store, on windows that are
+    not multiples of the 31 x 15 x 32 tile (halo lanes / rows, partial z
+    chunks) and with a core band; the zero-norm case leaves u unchanged."""
+    import torch
+    from paper_1905_03748_b200 import kernels as K
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    for shape, core in (((13, 11, 9), (0, 13)), ((70, 47, 65), (9, 61)),
+                        ((33, 16, 32), (0, 33)), ((2, 2, 2), (0, 2))):
+        u = torch.rand(shape, device="cuda", generator=gen)
+        g = torch.empty_like(u)
+        s0 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        K.tv_grad_store(u, g, core, s0)
+        # two-pass reference: step, then gradient of the stepped volume
+        u1 = torch.empty_like(u)
+        K.tv_step_g(u, g, u1, 0.05, s0, 1.3)
+        g1 = torch.empty_like(u)
+        s1 = torch.zeros_like(s0)
+        K.tv_grad_store(u1, g1, core, s1)
+        # fused
+        u2 = torch.empty_like(u)
+        g2 = torch.empty_like(u)
+        s2 = torch.zeros_like(s0)
+        K.tv_gd_fused(u, g, u2, g2, core, 0.05, s0, 1.3, s2)
+        assert torch.equal(u1, u2), shape
+        assert torch.equal(g1, g2), shape
+        assert torch.equal(s1, s2), shape
+    # flat volume: ||g|| = 0 -> the step is skipped (regularization.py:148)
+    u = torch.full((9, 10, 11), 0.25, device="cuda")
+    g = torch.empty_like(u)
+    s0 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    K.tv_grad_store(u, g, (0, 9), s0)
+    assert float(s0) == 0.0
+    u2, g2 = torch.empty_like(u), torch.empty_like(u)
+    s2 = torch.ones_like(s0)
+    K.tv_gd_fused(u, g, u2, g2, (0, 9), 0.05, s0, 1.0, s2)
+    assert torch.equal(u2, u) and float(s2) == 0.0
+
+
+def test_tv_gd_vs_oracle_tiles():
+    """minimize_tv_gradient (grad pass, fused passes, final step) against the
+    oracle on a volume spanning several 31 x 15 x 32 tiles with remainders,
+    plus a 1-iteration and a 2-iteration run (no / one fused pass)."""
+    rng = np.random.default_rng(11)
+    f = rng.random((70, 47, 65), dtype=np.float32)
+    vol = cs.Volume(cs.VoxelGrid(65, 47, 70), f)
+    for iters in (1, 2, 9):
+        got = cs.minimize_tv_gradient(
+            vol, cs.TvParams(cs.TvMinimizer.GRADIENT_DESCENT,
+                             inner_iters=iters, step=0.5)).data
+        want = O.minimize_tv_gradient(f, iters, 0.5)
+        assert rel_l2(got, want) <= TOL_OP, iters
+        assert rel_l2(got, f) > 1e-4  # the step moved u
+
+
+def test_tv_gd_fused_matches_tiled_kernel_subprocess():
+    """The marching kernel's g equals the r01 tiled kernel's (CS_TV_TILED=1)
+    bit for bit on a window with halo-tile remainders."""
+    import subprocess
+    import sys
+    code = (
+        "import torch,sys;sys.path.insert(0,'.');"
+        "from paper_1905_03748_b200 import kernels as K;"
+        "u=torch.rand((45,38,70),device='cuda',"
+        "generator=torch.Generator(device='cuda').manual_seed(3));"
+        "g=torch.empty_like(u);s=torch.zeros(1,dtype=torch.float64,"
+        "device='cuda');K.tv_grad_store(u,g,(4,40),s);"
+        "torch.save((g.cpu(),s.cpu()),sys.argv[1])")
+    import os
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as td:
+        outs = []
+        for tiled in ("0", "1"):
+            f = os.path.join(td, f"g{tiled}.pt")
+            env = dict(os.environ, CS_TV_TILED=tiled)
+            subprocess.run([sys.executable, "-c", code, f], cwd=root,
+                           env=env, check=True)
+            outs.append(torch_load(f))
+    (g0, s0), (g1, s1) = outs
+    assert (g0 == g1).all()
+    assert abs(float(s0) - float(s1)) <= 1e-12 * float(s1)
+
+
+def torch_load(path):
+    import torch
+    return torch.load(path)
 
 
 def test_randomised_geometries_vs_oracle():

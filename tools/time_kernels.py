@@ -29,10 +29,15 @@ ops = {
     "siddon": lambda: K.fwd_siddon(vol, g, (0, A), (0, n), y),
 }
 only = os.environ.get("PROF_ONLY")
-if not only or "tv_gd_iter" in only or "rof_iter" in only:
+TVOPS = ("tv_gd_iter", "rof_iter", "tv_grad", "tv_fused", "tv_step",
+         "tv_run10")
+if not only or any(k in only for k in TVOPS):
+    from paper_1905_03748_b200 import regularization as REG
     u2 = torch.empty_like(vol)
     g2 = torch.empty_like(vol)
     ss = torch.zeros(1, dtype=torch.float64, device=dev)
+    ss2 = torch.zeros(1, dtype=torch.float64, device=dev)
+    g3 = torch.empty_like(vol)
     p3 = torch.zeros((3, n, n, n), device=dev)
     q3 = torch.empty_like(p3)
 
@@ -41,26 +46,33 @@ if not only or "tv_gd_iter" in only or "rof_iter" in only:
         K.tv_step_g(vol, g2, u2, 1e-3, ss, 1.0)
 
     ops["tv_gd_iter"] = tv_gd
+    ops["tv_grad"] = lambda: K.tv_grad_store(vol, g2, (0, n), ss)
+    ops["tv_fused"] = lambda: K.tv_gd_fused(vol, g2, u2, g3, (0, n), 1e-3,
+                                            ss, 1.0, ss2)
+    ops["tv_step"] = lambda: K.tv_step_g(vol, g2, u2, 1e-3, ss, 1.0)
+    ops["tv_run10"] = lambda: REG._gd_iterations(vol, 10, 1e-3)
     ops["rof_iter"] = lambda: K.rof_iter(vol, p3, q3, 0.1)
 if only:
     ops = {k: v for k, v in ops.items() if k in only.split(",")}
 out = {}
 for name, fn in ops.items():
-    for _ in range(3 if name in ("tv_gd_iter", "rof_iter") else 1):
+    for _ in range(3 if name in TVOPS else 1):
         fn()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(True), torch.cuda.Event(True)
     s.record()
-    reps = R * 10 if name in ("tv_gd_iter", "rof_iter") else R
+    reps = R * 10 if name in TVOPS else R
     for _ in range(reps):
         fn()
     e.record()
     torch.cuda.synchronize()
     t = s.elapsed_time(e) / reps * 1e-3
-    if name in ("tv_gd_iter", "rof_iter"):
-        bpv = 12.0 if name == "tv_gd_iter" else 28.0
+    if name in TVOPS:
+        its = 10 if name == "tv_run10" else 1
+        bpv = 28.0 if name == "rof_iter" else 12.0
+        t /= its
         out[name] = {"ms": t * 1e3, "gvox_per_s": n ** 3 / t / 1e9,
-                     "frac_hbm": n ** 3 * bpv / t / 6550.7e9}
+                     "frac_hbm": n ** 3 * bpv / t / (bench.measured_peak()[0] * 1e9)}
     else:
         out[name] = {"ms": t * 1e3, "gups": A * n ** 3 / t / 1e9}
 print(json.dumps({"tag": os.environ.get("TAG", ""), **out}))
