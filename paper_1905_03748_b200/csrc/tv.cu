@@ -73,7 +73,9 @@ __global__ void __launch_bounds__(256)
 }
 
 // 1 / sqrt(gx^2 + gy^2 + gz^2 + eps) with the rounding order pinned (no
-// contraction freedom), so every GD kernel produces the same bits; the
+// contraction freedom; the p = g * inv products are likewise __fmul_rn so
+// they cannot fuse into the divergence), so every GD kernel produces the
+// same bits; the
 // argument is >= eps (normal), where the ftz approximation equals rsqrtf.
 __device__ __forceinline__ float tv_inv_norm(float gx, float gy, float gz) {
   const float n = __fadd_rn(
@@ -197,9 +199,9 @@ __global__ void __launch_bounds__(TV_TX * TV_TY)
         const float gyv = (f & 4u) ? pl0[k + TV_UX] - cc : 0.f;
         const float gzv = zlast ? 0.f : pl1[k] - cc;
         const float inv = tv_inv_norm(gxv, gyv, gzv);
-        px = gxv * inv;
-        py = gyv * inv;
-        pz = gzv * inv;
+        px = __fmul_rn(gxv, inv);
+        py = __fmul_rn(gyv, inv);
+        pz = __fmul_rn(gzv, inv);
       }
       spx[e] = px;
       spy[e] = py;
@@ -369,8 +371,8 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
     const float gyv = (uy - uc) * my;
     const float gzv = (un - uc) * mz;
     const float inv = tv_inv_norm(gxv, gyv, gzv);
-    const float px = gxv * inv, py = gyv * inv;
-    const float pz = (in_xy && z >= 0) ? gzv * inv : 0.f;
+    const float px = __fmul_rn(gxv, inv), py = __fmul_rn(gyv, inv);
+    const float pz = (in_xy && z >= 0) ? __fmul_rn(gzv, inv) : 0.f;
     spy[z & 1][w][lane] = py;
     su[(z + 1) & 1][w][lane] = un;
     __syncthreads();
@@ -400,6 +402,179 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
     partial[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x +
             blockIdx.x] = sm;
   }
+}
+
+// Paired variant (nx even, 8-byte aligned windows): lane l holds the voxel
+// pair x = x0 - 2 + 2l, +1 (float2 loads / stores, 60 x 14 outputs per CTA):
+// the pair's inner neighbours stay in registers, so per voxel half the
+// shuffles, shared-memory and global instructions and half the per-plane
+// loop overhead.  Same expressions (and bits) as tv_march_kernel.
+constexpr int TM2_OX = 60;
+constexpr int TM2_NS = 4;          // ring stages of 8-byte slots (48 KB
+constexpr int TM2_D = TM2_NS - 1;  // static shared memory when fused)
+
+__device__ __forceinline__ void cp_async8(unsigned dst, const float* src,
+                                          bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst),
+               "l"(src), "r"(ok ? 8 : 0)
+               : "memory");
+}
+
+template <int FUSED>
+__global__ void __launch_bounds__(TM_THREADS, 2)
+    tv_march2_kernel(const float* __restrict__ u,
+                     const float* __restrict__ gin, float* __restrict__ uo,
+                     float* __restrict__ gout, Win W, int c_lo, int c_hi,
+                     double step, const double* __restrict__ sumsq_in,
+                     double scale, double* __restrict__ partial) {
+  constexpr int NA = FUSED ? 2 : 1;
+  __shared__ float2 ring[TM2_NS][NA][TM_THREADS];
+  __shared__ float2 su[2][TM_WARPS][32];
+  __shared__ float2 spy[2][TM_WARPS][32];
+  double* sred = reinterpret_cast<double*>(&su[0][0][0]);  // after the loop
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tid = threadIdx.x;
+  const int x = blockIdx.x * TM2_OX - 2 + 2 * lane;  // pair (x, x + 1)
+  const int y = blockIdx.y * TM_OY - 1 + w;
+  const int zb = blockIdx.z * TM_ZC;
+  const int ze = min(W.nz, zb + TM_ZC);
+  // nx even, x even: the pair is wholly inside or wholly outside
+  const bool in_xy = x >= 0 && x < W.nx && y >= 0 && y < W.ny;
+  const bool own = in_xy && lane > 0 && lane < 31 && w > 0 && w < TM_WARPS - 1;
+  const size_t plane = (size_t)W.nx * W.ny;
+  const int off = in_xy ? y * W.nx + x : 0;
+  double coef = 0.0;
+  if (FUSED) {
+    const double norm = sqrt(*sumsq_in) * scale;
+    coef = norm < 1e-30 ? 0.0 : step / norm;  // regularization.py:148-149
+  }
+  const unsigned ring0 = (unsigned)__cvta_generic_to_shared(&ring[0][0][tid]);
+  constexpr unsigned RS = NA * TM_THREADS * 8, RA = TM_THREADS * 8;
+  int zi = zb - 1;
+  const float* pu = u + (ptrdiff_t)zi * (ptrdiff_t)plane + off;
+  const float* pg = FUSED ? gin + (ptrdiff_t)zi * (ptrdiff_t)plane + off : u;
+  auto issue = [&]() {
+    const bool ok = in_xy && (unsigned)zi < (unsigned)W.nz;
+    const unsigned st = ring0 + ((zi - zb + 1) & (TM2_NS - 1)) * RS;
+    cp_async8(st, ok ? pu : u, ok);
+    if (FUSED) cp_async8(st + RA, ok ? pg : u, ok);
+    cp_async_commit();
+    zi++;
+    pu += plane;
+    if (FUSED) pg += plane;
+  };
+  auto take = [&](int zz) {
+    const int st = (zz - zb + 1) & (TM2_NS - 1);
+    float2 v = ring[st][0][tid];
+    if (FUSED) {
+      const float2 gg = ring[st][NA - 1][tid];
+      v.x = (float)((double)v.x - coef * (double)gg.x);  // as tv_step_g
+      v.y = (float)((double)v.y - coef * (double)gg.y);
+    }
+    return v;
+  };
+#pragma unroll
+  for (int i = 0; i <= TM2_D - 1; i++) issue();
+  cp_async_wait<TM2_D - 1>();
+  float2 uc = take(zb - 1);
+  su[(zb - 1) & 1][w][lane] = uc;
+  __syncthreads();
+  float2 pz_prev = make_float2(0.f, 0.f);
+  double acc = 0.0;
+  float2* po = reinterpret_cast<float2*>(gout + (ptrdiff_t)zb * (ptrdiff_t)plane + off);
+  float2* puo = FUSED ? reinterpret_cast<float2*>(
+                            uo + (ptrdiff_t)zb * (ptrdiff_t)plane + off)
+                      : nullptr;
+  const size_t plane2 = plane / 2;
+  const int wy = w < TM_WARPS - 1 ? w + 1 : w;
+  const float mxa = in_xy ? 1.f : 0.f;  // x < nx - 1 holds for the even x
+  const float mxb = (in_xy && x + 1 < W.nx - 1) ? 1.f : 0.f;
+  const float my = (in_xy && y < W.ny - 1) ? 1.f : 0.f;
+  const int zlo_sum = max(zb, c_lo), zhi_sum = own ? c_hi : INT_MIN;
+  for (int z = zb - 1; z < ze; z++) {
+    issue();
+    cp_async_wait<TM2_D - 1>();
+    const float2 un = take(z + 1);
+    const float uxb = __shfl_down_sync(0xffffffffu, uc.x, 1);
+    const float2 uy = su[z & 1][wy][lane];
+    const float mz = (in_xy && z >= 0 && z < W.nz - 1) ? 1.f : 0.f;
+    const float gxa = (uc.y - uc.x) * mxa, gxb = (uxb - uc.y) * mxb;
+    const float gya = (uy.x - uc.x) * my, gyb = (uy.y - uc.y) * my;
+    const float gza = (un.x - uc.x) * mz, gzb = (un.y - uc.y) * mz;
+    const float ia = tv_inv_norm(gxa, gya, gza);
+    const float ib = tv_inv_norm(gxb, gyb, gzb);
+    const bool pv = in_xy && z >= 0;
+    const float pxa = __fmul_rn(gxa, ia), pxb = __fmul_rn(gxb, ib);
+    const float2 py = make_float2(__fmul_rn(gya, ia), __fmul_rn(gyb, ib));
+    const float2 pz = make_float2(pv ? __fmul_rn(gza, ia) : 0.f, pv ? __fmul_rn(gzb, ib) : 0.f);
+    spy[z & 1][w][lane] = py;
+    su[(z + 1) & 1][w][lane] = un;
+    __syncthreads();
+    const float pxm = __shfl_up_sync(0xffffffffu, pxb, 1);
+    const float2 pym = spy[z & 1][w > 0 ? w - 1 : 0][lane];
+    const float ga = -((pz.x - pz_prev.x) + (py.x - pym.x) + (pxa - pxm));
+    const float gb = -((pz.y - pz_prev.y) + (py.y - pym.y) + (pxb - pxa));
+    if (z >= zb) {
+      if (own) {
+        *po = make_float2(ga, gb);
+        if (FUSED) *puo = uc;
+      }
+      po += plane2;
+      if (FUSED) puo += plane2;
+    }
+    const bool sum = z >= zlo_sum && z < zhi_sum;
+    const float sa = sum ? ga : 0.f, sb = sum ? gb : 0.f;
+    acc += (double)sa * (double)sa;
+    acc += (double)sb * (double)sb;
+    pz_prev = pz;
+    uc = un;
+  }
+  cp_async_wait<0>();
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __syncthreads();  // su is reused for the warp sums
+  if (lane == 0) sred[w] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double sm = 0.0;
+    for (int i = 0; i < TM_WARPS; i++) sm += sred[i];
+    partial[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x +
+            blockIdx.x] = sm;
+  }
+}
+
+int reduce_into(const double* partial, size_t n, double* out, cudaStream_t s);
+
+// Launch the marching GD pass: the paired kernel when nx is even and every
+// buffer is 8-byte aligned, else the single-voxel kernel.
+template <int FUSED>
+static int launch_march(const float* u, const float* g, float* uo, float* go,
+                        int nx, int ny, int nzw, int core_lo, int core_hi,
+                        double step, const double* sumsq_in, double scale,
+                        double* out_sum, cudaStream_t s) {
+  static const char* knob = getenv("CS_TV_PAIRS");  // A/B: 0 = single
+  const bool pairs =
+      (!knob || knob[0] != '0') && nx % 2 == 0 && (uintptr_t)u % 8 == 0 &&
+      (uintptr_t)go % 8 == 0 &&
+      (!FUSED || ((uintptr_t)g % 8 == 0 && (uintptr_t)uo % 8 == 0));
+  const dim3 grid((nx + (pairs ? TM2_OX : TM_OX) - 1) / (pairs ? TM2_OX : TM_OX),
+                  (ny + TM_OY - 1) / TM_OY, (nzw + TM_ZC - 1) / TM_ZC);
+  const size_t nb = (size_t)grid.x * grid.y * grid.z;
+  double* part = nullptr;
+  retain_pool();
+  CS_CHECK_CUDA(cudaMallocAsync((void**)&part, nb * sizeof(double), s));
+  if (pairs)
+    tv_march2_kernel<FUSED><<<grid, TM_THREADS, 0, s>>>(
+        u, g, uo, go, Win{nx, ny, nzw}, core_lo, core_hi, step, sumsq_in,
+        scale, part);
+  else
+    tv_march_kernel<FUSED><<<grid, TM_THREADS, 0, s>>>(
+        u, g, uo, go, Win{nx, ny, nzw}, core_lo, core_hi, step, sumsq_in,
+        scale, part);
+  CS_COUNT_LAUNCH();
+  CS_CHECK_CUDA(cudaGetLastError());
+  const int rc = reduce_into(part, nb, out_sum, s);
+  cudaFreeAsync(part, s);
+  return rc;
 }
 
 // ---- ROF (regularization.py:154-182) ------------------------------------
@@ -650,20 +825,8 @@ int cs_tv_grad_store(const float* u, float* g, int nx, int ny, int nzw,
     cudaFreeAsync(part, s);
     return rc;
   }
-  const dim3 grid((nx + TM_OX - 1) / TM_OX, (ny + TM_OY - 1) / TM_OY,
-                  (nzw + TM_ZC - 1) / TM_ZC);
-  const size_t nb = (size_t)grid.x * grid.y * grid.z;
-  double* part = nullptr;
-  retain_pool();
-  CS_CHECK_CUDA(cudaMallocAsync((void**)&part, nb * sizeof(double), s));
-  tv_march_kernel<0><<<grid, TM_THREADS, 0, s>>>(
-      u, nullptr, nullptr, g, Win{nx, ny, nzw}, core_lo, core_hi, 0.0,
-      nullptr, 1.0, part);
-  CS_COUNT_LAUNCH();
-  CS_CHECK_CUDA(cudaGetLastError());
-  rc = reduce_into(part, nb, out_sum, s);
-  cudaFreeAsync(part, s);
-  return rc;
+  return launch_march<0>(u, nullptr, nullptr, g, nx, ny, nzw, core_lo,
+                         core_hi, 0.0, nullptr, 1.0, out_sum, s);
 }
 
 int cs_tv_gd_fused(const float* u, const float* g, float* u_out, float* g_out,
@@ -680,20 +843,8 @@ int cs_tv_gd_fused(const float* u, const float* g, float* u_out, float* g_out,
   CS_REQUIRE(norm_sumsq_dev != out_sum, CS_ERR_ARG,
              "cs_tv_gd_fused: the input and output sums must differ");
   cudaStream_t s = (cudaStream_t)stream;
-  const dim3 grid((nx + TM_OX - 1) / TM_OX, (ny + TM_OY - 1) / TM_OY,
-                  (nzw + TM_ZC - 1) / TM_ZC);
-  const size_t nb = (size_t)grid.x * grid.y * grid.z;
-  double* part = nullptr;
-  retain_pool();
-  CS_CHECK_CUDA(cudaMallocAsync((void**)&part, nb * sizeof(double), s));
-  tv_march_kernel<1><<<grid, TM_THREADS, 0, s>>>(
-      u, g, u_out, g_out, Win{nx, ny, nzw}, core_lo, core_hi, step,
-      norm_sumsq_dev, scale, part);
-  CS_COUNT_LAUNCH();
-  CS_CHECK_CUDA(cudaGetLastError());
-  rc = reduce_into(part, nb, out_sum, s);
-  cudaFreeAsync(part, s);
-  return rc;
+  return launch_march<1>(u, g, u_out, g_out, nx, ny, nzw, core_lo, core_hi,
+                         step, norm_sumsq_dev, scale, out_sum, s);
 }
 
 int cs_tv_step_g(const float* u, const float* g, float* u_out, int64_t n,

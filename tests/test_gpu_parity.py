@@ -761,8 +761,10 @@ def test_tv_gd_fused_bit_identical():
     import torch
     from paper_1905_03748_b200 import kernels as K
     gen = torch.Generator(device="cuda").manual_seed(7)
+    # odd nx: single-voxel kernel; even nx: paired kernel (60 x 14 tiles)
     for shape, core in (((13, 11, 9), (0, 13)), ((70, 47, 65), (9, 61)),
-                        ((33, 16, 32), (0, 33)), ((2, 2, 2), (0, 2))):
+                        ((33, 16, 32), (0, 33)), ((2, 2, 2), (0, 2)),
+                        ((70, 47, 126), (9, 61)), ((35, 29, 62), (0, 35))):
         u = torch.rand(shape, device="cuda", generator=gen)
         g = torch.empty_like(u)
         s0 = torch.zeros(1, dtype=torch.float64, device="cuda")
@@ -798,44 +800,51 @@ def test_tv_gd_vs_oracle_tiles():
     oracle on a volume spanning several 31 x 15 x 32 tiles with remainders,
     plus a 1-iteration and a 2-iteration run (no / one fused pass)."""
     rng = np.random.default_rng(11)
-    f = rng.random((70, 47, 65), dtype=np.float32)
-    vol = cs.Volume(cs.VoxelGrid(65, 47, 70), f)
-    for iters in (1, 2, 9):
+    for nx, iters in ((65, 1), (65, 2), (65, 9), (126, 9)):
+        f = rng.random((70, 47, nx), dtype=np.float32)
+        vol = cs.Volume(cs.VoxelGrid(nx, 47, 70), f)
         got = cs.minimize_tv_gradient(
             vol, cs.TvParams(cs.TvMinimizer.GRADIENT_DESCENT,
                              inner_iters=iters, step=0.5)).data
         want = O.minimize_tv_gradient(f, iters, 0.5)
-        assert rel_l2(got, want) <= TOL_OP, iters
+        assert rel_l2(got, want) <= TOL_OP, (nx, iters)
         assert rel_l2(got, f) > 1e-4  # the step moved u
 
 
 def test_tv_gd_fused_matches_tiled_kernel_subprocess():
-    """The marching kernel's g equals the r01 tiled kernel's (CS_TV_TILED=1)
-    bit for bit on a window with halo-tile remainders."""
+    """The marching kernels' g equals the r01 tiled kernel's (CS_TV_TILED=1)
+    bit for bit, paired (even nx) and single-voxel (CS_TV_PAIRS=0), on a
+    window with tile remainders; the fused pass agrees between the paired
+    and single-voxel kernels."""
+    import os
     import subprocess
     import sys
+    import tempfile
     code = (
         "import torch,sys;sys.path.insert(0,'.');"
         "from paper_1905_03748_b200 import kernels as K;"
-        "u=torch.rand((45,38,70),device='cuda',"
-        "generator=torch.Generator(device='cuda').manual_seed(3));"
+        "gen=torch.Generator(device='cuda').manual_seed(3);"
+        "u=torch.rand((45,38,70),device='cuda',generator=gen);"
         "g=torch.empty_like(u);s=torch.zeros(1,dtype=torch.float64,"
         "device='cuda');K.tv_grad_store(u,g,(4,40),s);"
-        "torch.save((g.cpu(),s.cpu()),sys.argv[1])")
-    import os
-    import tempfile
+        "u2=torch.empty_like(u);g2=torch.empty_like(u);s2=torch.zeros_like(s);"
+        "K.tv_gd_fused(u,g,u2,g2,(4,40),0.05,s,1.0,s2);"
+        "torch.save((g.cpu(),s.cpu(),u2.cpu(),g2.cpu()),sys.argv[1])")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     with tempfile.TemporaryDirectory() as td:
         outs = []
-        for tiled in ("0", "1"):
-            f = os.path.join(td, f"g{tiled}.pt")
-            env = dict(os.environ, CS_TV_TILED=tiled)
+        for tag, env_add in (("pairs", {}), ("single", {"CS_TV_PAIRS": "0"}),
+                             ("tiled", {"CS_TV_TILED": "1"})):
+            f = os.path.join(td, f"{tag}.pt")
+            env = dict(os.environ, **env_add)
             subprocess.run([sys.executable, "-c", code, f], cwd=root,
                            env=env, check=True)
             outs.append(torch_load(f))
-    (g0, s0), (g1, s1) = outs
-    assert (g0 == g1).all()
-    assert abs(float(s0) - float(s1)) <= 1e-12 * float(s1)
+    (gp, sp, up, g2p), (gs, ss, us, g2s), (gt, st, _, _) = outs
+    assert (gp == gs).all() and (gp == gt).all()
+    assert (up == us).all() and (g2p == g2s).all()
+    for s_ in (ss, st):
+        assert abs(float(sp) - float(s_)) <= 1e-12 * float(sp)
 
 
 def torch_load(path):
