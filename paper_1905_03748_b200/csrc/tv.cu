@@ -14,6 +14,7 @@
 // (147 vs 113 Gvox*it/s at 512^3 with pass 2 recomputing g, which
 // cs_tv_grad_sumsq + cs_tv_step still do).  ROF is one fused pass per iteration (28 B /
 // voxel-iteration) with neighbours through L1 (__ldg).
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 
@@ -274,7 +275,8 @@ constexpr int TM_OX = 30, TM_OY = TM_WARPS - 2;
 #endif
 constexpr int TM_ZC = CS_TM_ZC;
 constexpr int TM_NS = 8;         // ring stages (power of two)
-constexpr int TM_D = TM_NS - 1;  // planes in flight
+constexpr int TM_D = TM_NS;  // planes in flight (the ring slot reused is
+                               // the one taken an iteration earlier)
 
 __device__ __forceinline__ void cp_async4(unsigned dst, const float* src,
                                           bool ok) {
@@ -326,11 +328,13 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
   int zi = zb - 1;
   const float* pu = u + (ptrdiff_t)zi * (ptrdiff_t)plane + off;
   const float* pg = FUSED ? gin + (ptrdiff_t)zi * (ptrdiff_t)plane + off : u;
-  auto issue = [&]() {
+  auto issue = [&]() {  // planes past ze are not needed: empty group
     const bool ok = in_xy && (unsigned)zi < (unsigned)W.nz;
     const unsigned st = ring0 + ((zi - zb + 1) & (TM_NS - 1)) * RS;
-    cp_async4(st, ok ? pu : u, ok);
-    if (FUSED) cp_async4(st + RA, ok ? pg : u, ok);
+    if (zi <= ze) {
+      cp_async4(st, ok ? pu : u, ok);
+      if (FUSED) cp_async4(st + RA, ok ? pg : u, ok);
+    }
     cp_async_commit();
     zi++;
     pu += plane;
@@ -411,7 +415,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
 // loop overhead.  Same expressions (and bits) as tv_march_kernel.
 constexpr int TM2_OX = 60;
 constexpr int TM2_NS = 4;          // ring stages of 8-byte slots (48 KB
-constexpr int TM2_D = TM2_NS - 1;  // static shared memory when fused)
+constexpr int TM2_D = TM2_NS;  // static shared memory when fused)
 
 __device__ __forceinline__ void cp_async8(unsigned dst, const float* src,
                                           bool ok) {
@@ -453,11 +457,13 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
   int zi = zb - 1;
   const float* pu = u + (ptrdiff_t)zi * (ptrdiff_t)plane + off;
   const float* pg = FUSED ? gin + (ptrdiff_t)zi * (ptrdiff_t)plane + off : u;
-  auto issue = [&]() {
+  auto issue = [&]() {  // planes past ze are not needed: empty group
     const bool ok = in_xy && (unsigned)zi < (unsigned)W.nz;
     const unsigned st = ring0 + ((zi - zb + 1) & (TM2_NS - 1)) * RS;
-    cp_async8(st, ok ? pu : u, ok);
-    if (FUSED) cp_async8(st + RA, ok ? pg : u, ok);
+    if (zi <= ze) {
+      cp_async8(st, ok ? pu : u, ok);
+      if (FUSED) cp_async8(st + RA, ok ? pg : u, ok);
+    }
     cp_async_commit();
     zi++;
     pu += plane;
@@ -579,6 +585,11 @@ static int launch_march(const float* u, const float* g, float* uo, float* go,
 
 // ---- ROF (regularization.py:154-182) ------------------------------------
 
+__device__ __forceinline__ float rof_inv_mag(float qz, float qy, float qx) {
+  return __frcp_rn(fmaxf(
+      sqrtf(__fmaf_rn(qx, qx, __fmaf_rn(qy, qy, __fmul_rn(qz, qz)))), 1.f));
+}
+
 // div p at (x, y, z) with p = 0 outside the window / on the undefined face
 __device__ __forceinline__ float divp(const float* __restrict__ p,
                                       const Win& W, size_t vol, int x, int y,
@@ -629,31 +640,154 @@ __global__ void __launch_bounds__(256)
   const bool zl = z < W.nz - 1, zf = z > 0, yl = y < W.ny - 1, yf = y > 0;
   const bool xl = x < nx - 1, xf = x > 0;
   // u = f + lam div p at i and at the +1 neighbours (forward gradient)
-  const float uc = __ldg(fi) + lam * divp_at(pi, vol, plane, nx, zl, zf, yl,
-                                             yf, xl, xf);
+  const float uc = __fmaf_rn(lam, divp_at(pi, vol, plane, nx, zl, zf, yl, yf,
+                                          xl, xf), __ldg(fi));
   float gz = 0.f, gy = 0.f, gx = 0.f;
   if (zl)
-    gz = (__ldg(fi + plane) +
-          lam * divp_at(pi + plane, vol, plane, nx, z + 1 < W.nz - 1, true,
-                        yl, yf, xl, xf)) - uc;
+    gz = __fmaf_rn(lam, divp_at(pi + plane, vol, plane, nx, z + 1 < W.nz - 1,
+                                true, yl, yf, xl, xf), __ldg(fi + plane)) - uc;
   if (yl)
-    gy = (__ldg(fi + nx) +
-          lam * divp_at(pi + nx, vol, plane, nx, zl, zf, y + 1 < W.ny - 1,
-                        true, xl, xf)) - uc;
+    gy = __fmaf_rn(lam, divp_at(pi + nx, vol, plane, nx, zl, zf,
+                                y + 1 < W.ny - 1, true, xl, xf),
+                   __ldg(fi + nx)) - uc;
   if (xl)
-    gx = (__ldg(fi + 1) +
-          lam * divp_at(pi + 1, vol, plane, nx, zl, zf, yl, yf,
-                        x + 1 < nx - 1, true)) - uc;
-  float qz = __ldg(pi) + tau_over_lam * gz;
-  float qy = __ldg(pi + vol) + tau_over_lam * gy;
-  float qx = __ldg(pi + 2 * vol) + tau_over_lam * gx;
+    gx = __fmaf_rn(lam, divp_at(pi + 1, vol, plane, nx, zl, zf, yl, yf,
+                                x + 1 < nx - 1, true), __ldg(fi + 1)) - uc;
+  float qz = __fmaf_rn(tau_over_lam, gz, __ldg(pi));
+  float qy = __fmaf_rn(tau_over_lam, gy, __ldg(pi + vol));
+  float qx = __fmaf_rn(tau_over_lam, gx, __ldg(pi + 2 * vol));
   // p / max(1, |p|): one reciprocal (mag >= 1) instead of three IEEE
-  // divisions
-  const float inv = __frcp_rn(fmaxf(sqrtf(qz * qz + qy * qy + qx * qx), 1.f));
+  // divisions (rounding order pinned: rof_march2_kernel gives the same bits)
+  const float inv = rof_inv_mag(qz, qy, qx);
   float* po = pout + i;
-  po[0] = qz * inv;
-  po[vol] = qy * inv;
-  po[2 * vol] = qx * inv;
+  po[0] = __fmul_rn(qz, inv);
+  po[vol] = __fmul_rn(qy, inv);
+  po[2 * vol] = __fmul_rn(qx, inv);
+}
+
+// ---- marching ROF (production for even nx) -----------------------------
+// One dual iteration in one pass with the layout of tv_march2_kernel (lane
+// = voxel pair, warp = row, 60 x 14 outputs, column march in z over TM_ZC
+// planes, one barrier per plane): a thread loads f and p (pz, py, px) of its
+// pair one plane ahead through a cp.async ring, forms u(z+1) = f + lam div p
+// -- px(x-1) by shfl_up, py(y-1) from a shared row, pz(z) in registers --
+// then the forward gradient of u at plane z (u(x+2) by shfl_down, u(y+1)
+// from a shared row) and writes p' = (p + tau/lam grad u) / max(1, |.|).
+// Values of p on the faces where the forward difference is undefined (and
+// outside the window) are zeroed at load, which is the masking of divp_at;
+// same expressions and rounding as rof_iter_kernel, so the same bits.
+// 28 B / voxel: f and p read once, p' written once.
+constexpr int RM_NS = 4;
+constexpr int RM_D = RM_NS - 1;
+
+__global__ void __launch_bounds__(TM_THREADS, 2)
+    rof_march2_kernel(const float* __restrict__ f, const float* __restrict__ pin,
+                      float* __restrict__ pout, Win W, float lam,
+                      float tau_over_lam) {
+  extern __shared__ float2 rm_ring[];  // [RM_NS][4][TM_THREADS]: f pz py px
+  __shared__ float2 su[2][TM_WARPS][32];
+  __shared__ float2 spy[2][TM_WARPS][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tid = threadIdx.x;
+  const int x = blockIdx.x * TM2_OX - 2 + 2 * lane;  // pair (x, x + 1)
+  const int y = blockIdx.y * TM_OY - 1 + w;
+  const int zb = blockIdx.z * TM_ZC;
+  const int ze = min(W.nz, zb + TM_ZC);
+  const bool in_xy = x >= 0 && x < W.nx && y >= 0 && y < W.ny;
+  const bool own = in_xy && lane > 0 && lane < 31 && w > 0 && w < TM_WARPS - 1;
+  const size_t plane = (size_t)W.nx * W.ny;
+  const size_t vol = plane * (size_t)W.nz;
+  const int off = in_xy ? y * W.nx + x : 0;
+  const bool xlb = x + 1 < W.nx - 1;  // x < nx - 1 holds for the even x
+  const bool yl = y < W.ny - 1;
+  const unsigned ring0 = (unsigned)__cvta_generic_to_shared(&rm_ring[tid]);
+  constexpr unsigned RS = 4 * TM_THREADS * 8, RA = TM_THREADS * 8;
+  int zi = zb - 1;
+  const float* pf = f + (ptrdiff_t)zi * (ptrdiff_t)plane + off;
+  const float* pp = pin + (ptrdiff_t)zi * (ptrdiff_t)plane + off;
+  auto issue = [&]() {
+    const bool ok = in_xy && (unsigned)zi < (unsigned)W.nz;
+    const unsigned st = ring0 + ((zi - zb + 1) & (RM_NS - 1)) * RS;
+    cp_async8(st, ok ? pf : f, ok);
+    cp_async8(st + RA, ok ? pp : f, ok);
+    cp_async8(st + 2 * RA, ok ? pp + vol : f, ok);
+    cp_async8(st + 3 * RA, ok ? pp + 2 * vol : f, ok);
+    cp_async_commit();
+    zi++;
+    pf += plane;
+    pp += plane;
+  };
+  auto take = [&](int zz, float2& fv, float2& pz, float2& py, float2& px) {
+    const float2* r = rm_ring + ((zz - zb + 1) & (RM_NS - 1)) * 4 * TM_THREADS + tid;
+    fv = r[0];
+    pz = r[TM_THREADS];
+    py = r[2 * TM_THREADS];
+    px = r[3 * TM_THREADS];
+  };
+#pragma unroll
+  for (int i = 0; i <= RM_D - 1; i++) issue();  // planes zb-1 .. zb-2+D
+  float2 u0 = make_float2(0.f, 0.f);
+  float2 pz0 = make_float2(0.f, 0.f), py0 = pz0, px0 = pz0;
+  float2* po = reinterpret_cast<float2*>(pout + (ptrdiff_t)zb * (ptrdiff_t)plane + off);
+  const size_t plane2 = plane / 2, vol2 = vol / 2;
+  const int wy = w < TM_WARPS - 1 ? w + 1 : w;
+  const int wm = w > 0 ? w - 1 : 0;
+  for (int z = zb - 2; z < ze; z++) {
+    if (z + 1 + RM_D <= ze) {  // planes up to ze; empty groups keep the count
+      issue();
+    } else {
+      cp_async_commit();
+    }
+    cp_async_wait<RM_D>();  // plane z + 1 landed (own slots only)
+    float2 f1, pz1, py1, px1;
+    take(z + 1, f1, pz1, py1, px1);
+    spy[(z + 1) & 1][w][lane] = py1;
+    __syncthreads();
+    // u(z + 1) = f + lam div p (divp_at's terms and order): the voxel's own
+    // p is dropped on the faces where its forward difference is undefined;
+    // the backward neighbours' p (never on such a face) are zero-filled
+    // outside the window.  The dual step below uses the raw p, as
+    // rof_iter_kernel does.
+    const float2 pym = spy[(z + 1) & 1][wm][lane];
+    const float pxm = __shfl_up_sync(0xffffffffu, px1.y, 1);
+    const bool zl1 = z + 1 < W.nz - 1;
+    const float2 pz1m = zl1 ? pz1 : make_float2(0.f, 0.f);
+    const float2 py1m = yl ? py1 : make_float2(0.f, 0.f);
+    const float px1mb = xlb ? px1.y : 0.f;
+    const float da = ((pz1m.x - pz0.x) + (py1m.x - pym.x)) + (px1.x - pxm);
+    const float db = ((pz1m.y - pz0.y) + (py1m.y - pym.y)) + (px1mb - px1.x);
+    const float2 u1 = make_float2(__fmaf_rn(lam, da, f1.x),
+                                  __fmaf_rn(lam, db, f1.y));
+    // gradient of u at plane z and the projected dual step
+    if (z >= zb) {
+      const float uxb = __shfl_down_sync(0xffffffffu, u0.x, 1);
+      const float2 uy = su[z & 1][wy][lane];
+      const bool zl = z < W.nz - 1;
+      const float gza = zl ? u1.x - u0.x : 0.f, gzb = zl ? u1.y - u0.y : 0.f;
+      const float gya = yl ? uy.x - u0.x : 0.f, gyb = yl ? uy.y - u0.y : 0.f;
+      const float gxa = u0.y - u0.x, gxb = xlb ? uxb - u0.y : 0.f;
+      const float qza = __fmaf_rn(tau_over_lam, gza, pz0.x);
+      const float qzb = __fmaf_rn(tau_over_lam, gzb, pz0.y);
+      const float qya = __fmaf_rn(tau_over_lam, gya, py0.x);
+      const float qyb = __fmaf_rn(tau_over_lam, gyb, py0.y);
+      const float qxa = __fmaf_rn(tau_over_lam, gxa, px0.x);
+      const float qxb = __fmaf_rn(tau_over_lam, gxb, px0.y);
+      const float ia = rof_inv_mag(qza, qya, qxa);
+      const float ib = rof_inv_mag(qzb, qyb, qxb);
+      if (own) {
+        po[0] = make_float2(__fmul_rn(qza, ia), __fmul_rn(qzb, ib));
+        po[vol2] = make_float2(__fmul_rn(qya, ia), __fmul_rn(qyb, ib));
+        po[2 * vol2] = make_float2(__fmul_rn(qxa, ia), __fmul_rn(qxb, ib));
+      }
+      po += plane2;
+    }
+    su[(z + 1) & 1][w][lane] = u1;
+    u0 = u1;
+    pz0 = pz1;
+    py0 = py1;
+    px0 = px1;
+  }
+  cp_async_wait<0>();
 }
 
 __global__ void __launch_bounds__(256)
@@ -884,9 +1018,32 @@ int cs_rof_iter(const float* f, const float* p_in, float* p_out, int nx,
   if (rc) return rc;
   CS_REQUIRE(p_in != p_out, CS_ERR_ARG, "cs_rof_iter: p_in aliases p_out");
   CS_REQUIRE(lam > 0, CS_ERR_ARG, "lambda must be positive");
-  const dim3 grid((nx + 31) / 32, (ny + 7) / 8, nzw);
-  rof_iter_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(
-      f, p_in, p_out, Win{nx, ny, nzw}, (float)lam, (float)(ROF_TAU / lam));
+  cudaStream_t s = (cudaStream_t)stream;
+  static const char* knob = getenv("CS_ROF_MARCH");  // A/B: 0 = r01 kernel
+  const bool march = (!knob || knob[0] != '0') && nx % 2 == 0 &&
+                     (uintptr_t)f % 8 == 0 && (uintptr_t)p_in % 8 == 0 &&
+                     (uintptr_t)p_out % 8 == 0;
+  if (march) {
+    const size_t smem = (size_t)RM_NS * 4 * TM_THREADS * sizeof(float2);
+    static std::atomic<unsigned long long> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_done.load() & bit)) {
+      CS_CHECK_CUDA(cudaFuncSetAttribute(
+          rof_march2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+          (int)smem));
+      attr_done.fetch_or(bit);
+    }
+    const dim3 grid((nx + TM2_OX - 1) / TM2_OX, (ny + TM_OY - 1) / TM_OY,
+                    (nzw + TM_ZC - 1) / TM_ZC);
+    rof_march2_kernel<<<grid, TM_THREADS, smem, s>>>(
+        f, p_in, p_out, Win{nx, ny, nzw}, (float)lam, (float)(ROF_TAU / lam));
+  } else {
+    const dim3 grid((nx + 31) / 32, (ny + 7) / 8, nzw);
+    rof_iter_kernel<<<grid, dim3(32, 8), 0, s>>>(
+        f, p_in, p_out, Win{nx, ny, nzw}, (float)lam, (float)(ROF_TAU / lam));
+  }
   CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   return CS_OK;

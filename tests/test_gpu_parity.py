@@ -847,6 +847,50 @@ def test_tv_gd_fused_matches_tiled_kernel_subprocess():
         assert abs(float(sp) - float(s_)) <= 1e-12 * float(sp)
 
 
+def test_rof_vs_oracle_tiles():
+    """minimize_rof against the oracle on volumes spanning several 60 x 14 x
+    32 tiles (marching kernel, even nx) and with odd nx (r01 kernel)."""
+    rng = np.random.default_rng(12)
+    for nx in (126, 65):
+        f = rng.random((70, 47, nx), dtype=np.float32)
+        vol = cs.Volume(cs.VoxelGrid(nx, 47, 70), f)
+        got = cs.minimize_rof(vol, cs.TvParams(cs.TvMinimizer.ROF,
+                                               inner_iters=7, lam=0.3)).data
+        want = O.minimize_rof(f, 7, 0.3)
+        assert rel_l2(got, want) <= TOL_OP, nx
+        assert rel_l2(got, f) > 1e-3
+
+
+def test_rof_march_bit_identical_subprocess():
+    """The marching ROF kernel gives the r01 kernel's bits (CS_ROF_MARCH=0)
+    for a dual field that is nonzero everywhere, faces included (halo
+    windows carry interior p onto their faces), on a window with tile
+    remainders."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    code = (
+        "import torch,sys;sys.path.insert(0,'.');"
+        "from paper_1905_03748_b200 import kernels as K;"
+        "gen=torch.Generator(device='cuda').manual_seed(5);"
+        "f=torch.rand((45,38,70),device='cuda',generator=gen);"
+        "p=torch.rand((3,45,38,70),device='cuda',generator=gen)-0.5;"
+        "q=torch.empty_like(p);K.rof_iter(f,p,q,0.2);"
+        "q2=torch.empty_like(p);K.rof_iter(f,q,q2,0.2);"
+        "torch.save((q.cpu(),q2.cpu()),sys.argv[1])")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as td:
+        outs = []
+        for tag, env_add in (("march", {}), ("r01", {"CS_ROF_MARCH": "0"})):
+            fn = os.path.join(td, f"{tag}.pt")
+            subprocess.run([sys.executable, "-c", code, fn], cwd=root,
+                           env=dict(os.environ, **env_add), check=True)
+            outs.append(torch_load(fn))
+    (a1, a2), (b1, b2) = outs
+    assert (a1 == b1).all() and (a2 == b2).all()
+
+
 def torch_load(path):
     import torch
     return torch.load(path)
