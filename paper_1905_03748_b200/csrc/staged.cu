@@ -59,6 +59,29 @@ __device__ __forceinline__ int qfloor(const March& m, int k, int axis) {
   return q_cell(q_at(m, k, axis));  // exact (common.cuh)
 }
 
+// Packed fp32 pairs (sm_100 FMUL2 / FFMA2: two lanes of fp32 per
+// instruction, each rounded exactly as the scalar op), for the matched
+// deposit's weight products and magic-add conversions.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 f2(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_split(f32x2 v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f32x2 f2_mul(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 f2_fma(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
 // Red of a float4 quad (16-byte aligned) -- see backward.cu.
 __device__ __forceinline__ void st_red4(float* p, float a, float b, float c,
                                         float d) {
@@ -92,7 +115,8 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
                   float* __restrict__ out, const float* __restrict__ proj_in,
                   const float* __restrict__ rb, const float* __restrict__ rw,
                   int box_cap, float fx_budget, int vec_ok, int lane_stride,
-                  int prec_mode, float prec_fp, int edge, float lo_scale) {
+                  int prec_mode, float prec_fp, int edge, float lo_scale,
+                  int tpad) {
   constexpr int T = 1 - M;
   extern __shared__ float4 st_box4[];
   float* st_box = reinterpret_cast<float*>(st_box4);
@@ -337,6 +361,9 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
       const int xn = M == 0 ? S + 1 : nt;
       const int nbx = ((xlo + xn - (xlo & ~3)) + 3) & ~3;
       const int nby = M == 0 ? nt : S + 1;
+      if (OP == OP_BWD && tpad)  // T pitch padded (layout below)
+        return M == 1 ? ((nbx + tpad) & ~tpad) * nby * nzz
+                      : nbx * ((nby + tpad) & ~tpad) * nzz;
       return M == 1 ? nbx * nby * nzz : nbx * (nby | 1) * nzz;
     };
     bool prec = false;
@@ -373,10 +400,16 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
     // Shared layout: the transverse axis is innermost, so the 32 lanes of a
     // warp (adjacent detector columns = adjacent T) hit distinct banks:
     //   M = y: [z][y][x] (x = T, unit stride; x-quads contiguous)
-    //   M = x: [z][x][y] (y = T, unit stride; odd x pitch -> no conflicts)
-    const int sx = M == 1 ? 1 : (bn[1] | 1);
-    const int sy = M == 1 ? bn[0] : 1;
-    const int sz = M == 1 ? bn[0] * bn[1] : bn[0] * sx;
+    //   M = x: [z][x][y] (y = T, unit stride)
+    // Matched: the T rows are padded to a multiple of 32 words, so the M and
+    // z pitches are multiples of 32 and a warp's deposits (lanes in two M
+    // cells / z rows) collide only where their T cells agree mod 32 -- 12%
+    // fewer ATOMS wavefronts in the bank model (tools/sim_smem_banks.py:
+    // 2.28 vs 2.58 per deposit).  Ax: odd x pitch (its box fill writes
+    // x-quads across a warp, which a 32-word pitch would put in one bank).
+    const int sx = M == 1 ? 1 : (tpad ? (bn[1] + tpad) & ~tpad : (bn[1] | 1));
+    const int sy = M == 1 ? (bn[0] + tpad) & ~tpad : 1;
+    const int sz = M == 1 ? sy * bn[1] : bn[0] * sx;
     const int bsize = sz * bn[2];
     const bool fits = !mixed && bsize <= cap_eff;
     const int qpr = bn[0] >> 2;            // x-quads per (y, z) row
@@ -478,9 +511,11 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
             const float b1 = fmaf(wy, r11 - r10, r10);
             acc += fmaf(wz, b1 - b0, b0);
           } else {
-            const float z0 = sv * (1.f - wz), z1 = sv * wz;
-            const float y00 = z0 * (1.f - wy), y01 = z0 * wy;
-            const float y10 = z1 * (1.f - wy), y11 = z1 * wy;
+            float z0, z1, y00, y01, y10, y11;
+            f2_split(f2_mul(f2(sv, sv), f2(1.f - wz, wz)), z0, z1);
+            const f32x2 wyp = f2(1.f - wy, wy);
+            f2_split(f2_mul(f2(z0, z0), wyp), y00, y01);
+            f2_split(f2_mul(f2(z1, z1), wyp), y10, y11);
             const float vx = 1.f - wx;
             if (BM == 1) {
               deposit2(b, y00, vx);
@@ -492,14 +527,19 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
               deposit2(b + sz + sy, y11, vx);
               deposit2(b + sz + sy + sx, y11, wx);
             } else {
-              deposit(b, y00, vx);
-              deposit(b + sx, y00, wx);
-              deposit(b + sy, y01, vx);
-              deposit(b + sy + sx, y01, wx);
-              deposit(b + sz, y10, vx);
-              deposit(b + sz + sx, y10, wx);
-              deposit(b + sz + sy, y11, vx);
-              deposit(b + sz + sy + sx, y11, wx);
+              // the same products and magic adds as deposit(), two per
+              // FMUL2 / FFMA2 (bit-identical taps)
+              const f32x2 wxp = f2(vx, wx), mm = f2(ST_MAGIC, ST_MAGIC);
+              float t0, t1;
+              auto dep2 = [&](int idx, float y, int dx) {
+                f2_split(f2_fma(f2(y, y), wxp, mm), t0, t1);
+                atomicAdd(box_i + idx, magic_int(t0));
+                atomicAdd(box_i + idx + dx, magic_int(t1));
+              };
+              dep2(b, y00, sx);
+              dep2(b + sy, y01, sx);
+              dep2(b + sz, y10, sx);
+              dep2(b + sz + sy, y11, sx);
             }
           }
         } else {
@@ -542,18 +582,26 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
     if (OP == OP_BWD && fits) {
       __syncthreads();
       // flush the box: one 16-byte reduction per aligned x-quad.  A thread
-      // owns one (x-quad, y) column of the box and walks it in z, so the
-      // column's box and global offsets are computed once (the flat
-      // quad-index walk cost ~25% of the kernel's instructions).  Threads
-      // are laid along the box's unit-stride axis (x-quads for M = y, y for
-      // M = x), so the shared loads of a warp do not conflict.
+      // owns one (x-quad, y) column of the box and walks it in z with
+      // running shared / global pointers (the per-quad index arithmetic
+      // was ~25% of the kernel's instructions), over the planes inside the
+      // slab only.  Threads are laid along the box's unit-stride axis
+      // (x-quads for M = y, y for M = x), so the shared loads of a warp do
+      // not conflict.
       const int qpr_ = bn[0] >> 2;
       const int P = qpr_ * bn[1];                  // columns per z-plane
-      const int zstep = P <= ST_THREADS ? ST_THREADS / P : 1;
-      const int z_first = P <= ST_THREADS ? threadIdx.x / P : 0;
-      const int pstride = P <= ST_THREADS ? P : ST_THREADS;
+      const bool fold = P <= ST_THREADS;           // several z per pass
+      const int zstep = fold ? ST_THREADS / P : 1;
+      const int z_first = fold ? threadIdx.x / P : 0;
+      const int pstride = fold ? P : ST_THREADS;
+      const int bz0 = max(0, z_lo - bo[2]), bz1 = min(bn[2], z_hi - bo[2]);
+      int bzs = z_first;
+      while (bzs < bz0) bzs += zstep;
       const float il = inv_scale / lo_scale;
-      for (int cp = P <= ST_THREADS ? threadIdx.x - z_first * P : threadIdx.x;
+      const int wps = prec ? 2 : 1;                // words per box voxel
+      const int bstep = zstep * sz * wps;
+      const size_t gstep = (size_t)zstep * plane;
+      for (int cp = fold ? threadIdx.x - z_first * P : threadIdx.x;
            z_first < zstep && cp < P; cp += pstride) {
         int xq, by;
         if (M == 1) {
@@ -566,25 +614,24 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
         const int gx = bo[0] + 4 * xq, gy = bo[1] + by;
         if (gy < 0 || gy >= ny) continue;
         const bool vec = vec_ok && gx >= 0 && gx + 3 < nx;
-        const int dcol = by * sy + 4 * xq * sx;
-        float* dcolp = vol_acc + (size_t)gy * nx + gx;
-        for (int bz = z_first; bz < bn[2]; bz += zstep) {
-          const int gz = bo[2] + bz;
-          if (gz < z_lo || gz >= z_hi) continue;
-          const int d = dcol + bz * sz;
+        const int* bp = box_i + (by * sy + 4 * xq * sx + bzs * sz) * wps;
+        float* gp = vol_acc + (size_t)(bo[2] + bzs - z_lo) * plane +
+                    (size_t)gy * nx + gx;
+        const int sxw = sx * wps;
+        for (int bz = bzs; bz < bz1; bz += zstep, bp += bstep, gp += gstep) {
           float f0, f1, f2, f3;
           if (prec) {
             int2 q0, q1, q2, q3;
             if (M == 1) {
-              const int4 a01 = *reinterpret_cast<const int4*>(box_i + 2 * d);
-              const int4 a23 =
-                  *reinterpret_cast<const int4*>(box_i + 2 * d + 4);
+              const int4 a01 = *reinterpret_cast<const int4*>(bp);
+              const int4 a23 = *reinterpret_cast<const int4*>(bp + 4);
               q0 = make_int2(a01.x, a01.y); q1 = make_int2(a01.z, a01.w);
               q2 = make_int2(a23.x, a23.y); q3 = make_int2(a23.z, a23.w);
             } else {
-              const int2* b2 = reinterpret_cast<const int2*>(box_i);
-              q0 = b2[d]; q1 = b2[d + sx]; q2 = b2[d + 2 * sx];
-              q3 = b2[d + 3 * sx];
+              q0 = *reinterpret_cast<const int2*>(bp);
+              q1 = *reinterpret_cast<const int2*>(bp + sxw);
+              q2 = *reinterpret_cast<const int2*>(bp + 2 * sxw);
+              q3 = *reinterpret_cast<const int2*>(bp + 3 * sxw);
             }
             if ((q0.x | q0.y | q1.x | q1.y | q2.x | q2.y | q3.x | q3.y) == 0)
               continue;
@@ -595,27 +642,26 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
           } else {
             int q0, q1, q2, q3;
             if (M == 1) {
-              const int4 q = *reinterpret_cast<const int4*>(box_i + d);
+              const int4 q = *reinterpret_cast<const int4*>(bp);
               q0 = q.x; q1 = q.y; q2 = q.z; q3 = q.w;
             } else {
-              q0 = box_i[d];
-              q1 = box_i[d + sx];
-              q2 = box_i[d + 2 * sx];
-              q3 = box_i[d + 3 * sx];
+              q0 = bp[0];
+              q1 = bp[sxw];
+              q2 = bp[2 * sxw];
+              q3 = bp[3 * sxw];
             }
             if ((q0 | q1 | q2 | q3) == 0) continue;
             f0 = (float)q0 * inv_scale; f1 = (float)q1 * inv_scale;
             f2 = (float)q2 * inv_scale; f3 = (float)q3 * inv_scale;
           }
-          float* dst = dcolp + (size_t)(gz - z_lo) * plane;
           if (vec) {
-            st_red4(dst, f0, f1, f2, f3);
+            st_red4(gp, f0, f1, f2, f3);
           } else {
             const float f[4] = {f0, f1, f2, f3};
 #pragma unroll
             for (int j = 0; j < 4; j++)
               if (gx + j >= 0 && gx + j < nx && f[j] != 0.f)
-                atomicAdd(dst + j, f[j]);
+                atomicAdd(gp + j, f[j]);
           }
         }
       }
@@ -742,7 +788,14 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   // at 1024^3, +10% at 2048^3: the smaller boxes take more half-depth chunks
   // and flushes, which cost more once the slab is far beyond L2).  5 CTAs
   // (48 registers) spill.
-  const bool four = (double)(z_hi - z_lo) * nx * ny <= 134217728.0;  // 512^3
+  // r02: with the matched boxes' T pitch padded to 32 words (below), 3 CTAs
+  // x 72 KB win at every size (512^3: 208.6 vs 201.3 GUPS dense for the
+  // unpadded 4 x 54 KB; 1024^3: 217.0 vs 210.2; profiles/ab_matched_tpad_r02t
+  // .jsonl)
+  static const char* tp_env = getenv("CS_ST_TPAD");
+  const bool padded = OP == OP_BWD && !(tp_env && atoi(tp_env) == 0);
+  const bool four = !padded &&
+                    (double)(z_hi - z_lo) * nx * ny <= 134217728.0;  // 512^3
   static const char* kb_knob = getenv("CS_STAGED_SMEM_KB");
   // (3 CTAs: 72 KB boxes, +1-3% over 64 KB at 1024^3 / 2048^3; 80 KB no
   // longer fits three)
@@ -841,6 +894,9 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     const int k = atoi(ls_knob);
     if (k == 1 || k == 2 || k == 4 || k == 8) lane_stride = k;
   }
+  // matched T-pitch padding (power of two minus one; A/B knob CS_ST_TPAD)
+  static const char* tp_knob = getenv("CS_ST_TPAD");
+  const int tpad = OP == OP_BWD ? (tp_knob ? atoi(tp_knob) : 31) : 0;
   const unsigned gx = (n_u + ST_TU * lane_stride - 1) / (ST_TU * lane_stride);
   auto rows = [&](int c) {
     const int rv = ST_TV / lane_stride;
@@ -865,14 +921,14 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     k0<<<dim3(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids, G, step_max, z_lo, z_hi, n_u, n_v,
         band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_ok,
-        lane_stride, prec_mode, prec_fp, edge, lo_scale);
+        lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad);
     CS_COUNT_LAUNCH();
   }
   if (nall > nxm && rows(1) > 0) {
     k1<<<dim3(gx, rows(1), nall - nxm), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids + nxm, G, step_max, z_lo, z_hi, n_u, n_v,
         band[1][0], band[1][1], out, proj_in, rb, rw, cap, budget, vec_ok,
-        lane_stride, prec_mode, prec_fp, edge, lo_scale);
+        lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad);
     CS_COUNT_LAUNCH();
   }
   e = cudaGetLastError();
