@@ -223,12 +223,13 @@ def split_minimize(volume: Volume, pool: DevicePool, params: TvParams,
                                             params, rank)
         return _wrap(volume, u)
     # all windows on one device when they fit beside the volume (GD: u, the
-    # snapshot, windows, spares, stored g ~ 5 volumes; ROF: f, p, snapshot
-    # ~ 7), else the windows stream through host memory one at a time
-    # (the reference's bound: one window plus its copies, :197-210)
+    # snapshot, windows, spares, two stored g for the fused passes ~ 6
+    # volumes; ROF: f, p, snapshot ~ 7), else the windows stream through
+    # host memory one at a time (the reference's bound: one window plus its
+    # copies, :197-210)
     grid = volume.grid
     vol_bytes = grid.n_x * grid.n_y * (grid.n_z + 2 * d * len(slabs)) * 4
-    copies = 5 if params.minimizer is TvMinimizer.GRADIENT_DESCENT else 7
+    copies = 6 if params.minimizer is TvMinimizer.GRADIENT_DESCENT else 7
     fits = copies * vol_bytes <= usable_fraction * pool.min_budget
     if not volume.on_device and len(slabs) > 1 and not fits:
         host = np.ascontiguousarray(to_host(volume.data), np.float32)
