@@ -681,8 +681,7 @@ def run_extras(args, cs, K, g, vol, y, dev):
         t = rate(fn, 5) / its
         out[f"{name}_gvox_iter_per_s"] = vol.numel() / t / 1e9
         out[f"{name}_hbm_frac"] = vol.numel() * bpv / t / (peak * 1e9)
-    del u2, g3, ss2
-    del u2, g2, p3, q3, acc
+    del u2, g2, g3, ss2, p3, q3, acc
 
     # end-to-end through the public API with pinned host buffers:
     # Ax(volume host) -> projections host; Atb(dense stack host) -> volume

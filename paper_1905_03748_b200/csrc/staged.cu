@@ -41,6 +41,9 @@ constexpr int ST_THREADS = ST_TU * ST_TV;
 #ifndef CS_ST_S
 #define CS_ST_S 8
 #endif
+#ifndef CS_ST_ACC
+#define CS_ST_ACC 0
+#endif
 constexpr int ST_S = CS_ST_S;  // planes per chunk along the main axis
 
 
@@ -491,6 +494,23 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
         qy -= (long long)bo[1] << QF;
         qz -= (long long)bo[2] << QF;
       }
+#if CS_ST_ACC
+      // (A/B) consecutive samples of a ray in the same cell: their fixed-
+      // point taps are summed in registers and deposited when the cell
+      // changes (integer sums: the same bits as per-sample deposits)
+      int b_cur = -1;
+      int a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0, a7 = 0;
+      auto flush_acc = [&]() {
+        atomicAdd(box_i + b_cur, a0);
+        atomicAdd(box_i + b_cur + sx, a1);
+        atomicAdd(box_i + b_cur + sy, a2);
+        atomicAdd(box_i + b_cur + sy + sx, a3);
+        atomicAdd(box_i + b_cur + sz, a4);
+        atomicAdd(box_i + b_cur + sz + sx, a5);
+        atomicAdd(box_i + b_cur + sz + sy, a6);
+        atomicAdd(box_i + b_cur + sz + sy + sx, a7);
+      };
+#endif
       for (int kk = ka; kk < kb;
            kk++, qx += m.Bq[0], qy += m.Bq[1], qz += m.Bq[2]) {
         const float wx = q_frac(qx), wy = q_frac(qy), wz = q_frac(qz);
@@ -531,6 +551,23 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
               // FMUL2 / FFMA2 (bit-identical taps)
               const f32x2 wxp = f2(vx, wx), mm = f2(ST_MAGIC, ST_MAGIC);
               float t0, t1;
+#if CS_ST_ACC
+              if (b != b_cur) {
+                if (b_cur >= 0) flush_acc();
+                b_cur = b;
+                a0 = a1 = a2 = a3 = a4 = a5 = a6 = a7 = 0;
+              }
+              auto acc2 = [&](float y, int& lo, int& hi) {
+                f2_split(f2_fma(f2(y, y), wxp, mm), t0, t1);
+                lo += magic_int(t0);
+                hi += magic_int(t1);
+              };
+              acc2(y00, a0, a1);
+              acc2(y01, a2, a3);
+              acc2(y10, a4, a5);
+              acc2(y11, a6, a7);
+              continue;
+#endif
               auto dep2 = [&](int idx, float y, int dx) {
                 f2_split(f2_fma(f2(y, y), wxp, mm), t0, t1);
                 atomicAdd(box_i + idx, magic_int(t0));
@@ -570,6 +607,9 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
           }
         }
       }
+#if CS_ST_ACC
+      if (OP == OP_BWD && BM == 0 && b_cur >= 0) flush_acc();
+#endif
     };
     if (any) {
       if (!fits)

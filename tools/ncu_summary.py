@@ -28,6 +28,11 @@ METRICS = [
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy %"),
     ("launch__registers_per_thread", "regs"),
     ("smsp__inst_executed.sum", "warp insts"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+     "ATOMS wavefronts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum",
+     "ATOMS bank conflicts"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared wavefronts"),
 ]
 # kernel-name fragment -> bench key.  One Ax call on main-axis layers is
 # fill_xlayers + fwd_mlayer<.., 0> + fill_ylayers + fwd_mlayer<.., 1>: the
@@ -37,7 +42,10 @@ KEYS = {"fwd_mlayer": "fwd_mlayer_kernel", "fill_xlayers": "fwd_mlayer_kernel",
         "fwd_interp": "fwd_interp_kernel",
         "staged_kernel<1": "bwd_matched_kernel",
         "bwd_fdk": "bwd_fdk_kernel", "fdk_staged": "bwd_fdk_kernel",
-        "fwd_siddon": "fwd_siddon_kernel"}
+        "fwd_siddon": "fwd_siddon_kernel",
+        "tv_march2_kernel<1": "tv_gd_fused_kernel",
+        "tv_march2_kernel<0": "tv_grad_kernel",
+        "rof_march2": "rof_iter_kernel"}
 
 
 def to_bytes(v, unit):

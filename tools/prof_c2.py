@@ -20,23 +20,28 @@ dev = torch.device("cuda", 0)
 vol = cs.phantom(cs.PhantomKind.SHEPP_LOGAN_3D, g.voxel_grid, device=dev).data
 y = torch.empty((A, n, n), device=dev)
 K.fwd_interp(vol, g, (0, A), (0, n), y)
+# the bench's matched input: a dense standard-normal stack (bench.py)
+dense = torch.randn((C, n, n), device=dev, generator=torch.Generator(
+    device=dev).manual_seed(1))
 acc = torch.zeros((n, n, n), device=dev)
 proj = torch.empty((C, n, n), device=dev)
 u2 = torch.empty_like(vol)
 g2 = torch.empty_like(vol)
 ss = torch.zeros(1, dtype=torch.float64, device=dev)
+ss2 = torch.zeros(1, dtype=torch.float64, device=dev)
+g3 = torch.empty_like(vol)
 p3 = torch.zeros((3, n, n, n), device=dev)
 q3 = torch.empty_like(p3)
 torch.cuda.synchronize()
 for rep in range(2):
-    if "tv" in which:
+    if "tv" in which:  # GD: gradient pass, fused pass; ROF: dual iteration
         K.tv_grad_store(vol, g2, (0, n), ss)
-        K.tv_step_g(vol, g2, u2, 1e-3, ss, 1.0)
+        K.tv_gd_fused(vol, g2, u2, g3, (0, n), 1e-3, ss, 1.0, ss2)
         K.rof_iter(vol, p3, q3, 0.1)
     if "fwd" in which:
         K.fwd_interp(vol, g, (0, C), (0, n), proj)
     if "matched" in which:
-        K.bwd_matched(y[0:C], g, (0, C), (0, n), acc)
+        K.bwd_matched(dense, g, (0, C), (0, n), acc)
     if "fdk" in which:
         K.bwd_fdk(y[0:C], g, (0, C), (0, n), acc)
     if "siddon" in which:
