@@ -346,6 +346,22 @@ def test_out_of_core_loops_match_in_core():
     o_in = cs.os_sart(b, g, cfg_in).data
     o_out = cs.os_sart(b, g, cfg_out).data
     assert rel_l2(o_out, o_in) <= TOL_LOOP
+    # the host loop's float32 vectors with V_S recomputed per block instead
+    # of stored (HOST_WEIGHT_FRACTION = 0), and SART-TV out of core
+    from paper_1905_03748_b200 import algorithms as ALG
+    old = ALG.HOST_WEIGHT_FRACTION
+    ALG.HOST_WEIGHT_FRACTION = 0.0
+    try:
+        o_re = cs.os_sart(b, g, cfg_out).data
+    finally:
+        ALG.HOST_WEIGHT_FRACTION = old
+    assert rel_l2(o_re, o_in) <= TOL_LOOP
+    tv = cs.TvParams(cs.TvMinimizer.GRADIENT_DESCENT, 1, 4, 1e-3)
+    t_in = cs.os_sart(b, g, cs.ReconConfig(big, cs.Algorithm.OSSART, 2, 4,
+                                           tv=tv)).data
+    t_out = cs.os_sart(b, g, cs.ReconConfig(small, cs.Algorithm.OSSART, 2, 4,
+                                            tv=tv)).data
+    assert rel_l2(t_out, t_in) <= TOL_LOOP
 
 
 def _odd_geometry(nx, ny, nz, nu, nv, na, voxel=(1.0, 0.9, 1.1),
