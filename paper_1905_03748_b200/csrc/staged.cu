@@ -794,6 +794,29 @@ static size_t staged_smem_cap() {
   return cap;
 }
 
+// vol[z][y][x] += acc_t[z][x][y] over a slab (32 x 32 tiles through shared
+// memory, coalesced on both sides): the x-major views' matched Atb, computed
+// in the transposed frame, added into the volume (launch_staged).
+__global__ void __launch_bounds__(256)
+    transpose_add_kernel(float* __restrict__ vol,
+                         const float* __restrict__ acc_t, int nx, int ny) {
+  __shared__ float tile[32][33];
+  const size_t plane = (size_t)nx * ny;
+  const float* src = acc_t + (size_t)blockIdx.z * plane;
+  float* dst = vol + (size_t)blockIdx.z * plane;
+  const int x0 = blockIdx.y * 32, y0 = blockIdx.x * 32;
+  // read acc_t rows x (length ny), columns y
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int x = x0 + i, y = y0 + threadIdx.x;
+    tile[i][threadIdx.x] = (x < nx && y < ny) ? src[(size_t)x * ny + y] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int y = y0 + i, x = x0 + threadIdx.x;
+    if (x < nx && y < ny) dst[(size_t)y * nx + x] += tile[threadIdx.x][i];
+  }
+}
+
 // Launch one staged pass over n_a views (OP_FWD: Ax into out with MODE
 // epilogue; OP_BWD: matched Atb into vol_acc).
 template <int OP, int MODE>
@@ -957,7 +980,74 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
                            200 * 1024);
     attr_done.fetch_or(bit);
   }
-  if (nxm > 0 && rows(0) > 0) {
+  // Matched, x-major views: run them as y-major views of the transposed
+  // frame (x <-> y swapped in the geometry and grid) into a transposed slab
+  // accumulator, then add it back transposed.  The sample positions, taps
+  // and box sums are exactly those of the direct launch (the fp64 set-up is
+  // symmetric in x and y); only the fp32 summation into the volume is
+  // grouped differently.  The y-major layout flushes x-quads with one
+  // LDS.128 and contiguous REDs, where the x-major one needs four LDS and
+  // spreads a warp's REDs over 32 rows: 34.2 vs 24.3 ms per 45 views at
+  // 512^3 (profiles/ncu_r02w.md).  Needs a slab-sized buffer: used when the
+  // device has room for it (knob CS_ST_TRANSPOSE=0 disables).
+  bool transposed = false;
+  if (OP == OP_BWD && nxm > 0 && rows(0) > 0) {
+    static const char* tk = getenv("CS_ST_TRANSPOSE");
+    const size_t slab_bytes = (size_t)(z_hi - z_lo) * nx * ny * sizeof(float);
+    size_t free_b = 0, total_b = 0;
+    if (!(tk && tk[0] == '0') &&
+        cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
+        free_b > 2 * slab_bytes + ((size_t)2 << 30)) {
+      double* geom_t = (double*)malloc(sizeof(double) * 12 * (size_t)n_a);
+      memcpy(geom_t, geom, sizeof(double) * 12 * (size_t)n_a);
+      for (int a = 0; a < n_a; a++)
+        for (int c = 0; c < 12; c += 3) {
+          double* g3 = geom_t + 12 * a + c;
+          const double t = g3[0];
+          g3[0] = g3[1];
+          g3[1] = t;
+        }
+      double grid6_t[6] = {grid6[1], grid6[0], grid6[2],
+                           grid6[4], grid6[3], grid6[5]};
+      const Grid GT = make_grid(grid6_t, ny, nx, nz);
+      AngleGeom* dgeom_t = nullptr;
+      float* acc_t = nullptr;
+      rc = upload_geometry(geom_t, n_a, s, &dgeom_t);
+      free(geom_t);
+      cudaError_t e2 = rc ? cudaErrorUnknown
+                          : cudaMallocAsync((void**)&acc_t, slab_bytes, s);
+      if (!rc && e2 == cudaSuccess)
+        e2 = cudaMemsetAsync(acc_t, 0, slab_bytes, s);
+      if (!rc && e2 == cudaSuccess) {
+        const int vec_t = (ny % 4 == 0);
+        k1<<<dim3(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
+            vol_in, acc_t, dgeom_t, ids, GT, step_max, z_lo, z_hi, n_u, n_v,
+            band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_t,
+            lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad);
+        CS_COUNT_LAUNCH();
+        const dim3 tg((ny + 31) / 32, (nx + 31) / 32, z_hi - z_lo);
+        transpose_add_kernel<<<tg, dim3(32, 8), 0, s>>>(vol_acc, acc_t, nx,
+                                                        ny);
+        CS_COUNT_LAUNCH();
+        const cudaError_t e3 = cudaGetLastError();
+        cudaFreeAsync(acc_t, s);
+        release_geometry(dgeom_t, s);
+        if (e3 != cudaSuccess) {  // a launch failure is an error, not a
+          cudaFreeAsync(ids, s);  // fallback
+          release_geometry(dgeom, s);
+          CS_CHECK_CUDA(e3);
+        }
+        transposed = true;
+      } else {
+        // could not stage the transposed frame: the direct launch below
+        if (acc_t) cudaFreeAsync(acc_t, s);
+        if (dgeom_t) release_geometry(dgeom_t, s);
+        (void)cudaGetLastError();
+        rc = 0;
+      }
+    }
+  }
+  if (!transposed && nxm > 0 && rows(0) > 0) {
     k0<<<dim3(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids, G, step_max, z_lo, z_hi, n_u, n_v,
         band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_ok,

@@ -907,6 +907,45 @@ def test_rof_march_bit_identical_subprocess():
     assert (a1 == b1).all() and (a2 == b2).all()
 
 
+def test_matched_transposed_frame_subprocess():
+    """Matched Atb's x-major views run as y-major views of the transposed
+    frame (staged.cu); the direct x-major launch (CS_ST_TRANSPOSE=0) gives
+    the same box sums, so the two agree to fp32 summation order -- on odd,
+    non-multiple-of-4 sizes with anisotropic voxels, offsets and a slab."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    code = (
+        "import torch,sys,math,numpy as np;sys.path.insert(0,'.');"
+        "sys.path.insert(0,'tests');"
+        "import paper_1905_03748_b200 as cs;"
+        "from paper_1905_03748_b200 import kernels as K;"
+        "grid=cs.VoxelGrid(37,29,23,(1.0,0.9,1.1),(0.3,-0.2,0.1));"
+        "det=cs.DetectorGrid(41,27,(2.1,2.3),(0.4,-0.3));"
+        "ang=tuple(np.linspace(0.1,0.1+2*math.pi,19,endpoint=False));"
+        "g=cs.ScanGeometry(90.0,180.0,ang,grid,det);"
+        "y=torch.randn((19,27,41),device='cuda',"
+        "generator=torch.Generator(device='cuda').manual_seed(2));"
+        "acc=torch.zeros((23,29,37),device='cuda');"
+        "K.bwd_matched(y,g,(0,19),(0,23),acc);"
+        "sl=torch.zeros((9,29,37),device='cuda');"
+        "K.bwd_matched(y,g,(0,19),(7,16),sl);"
+        "torch.save((acc.cpu(),sl.cpu()),sys.argv[1])")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as td:
+        outs = []
+        for tag, env_add in (("t", {}), ("direct", {"CS_ST_TRANSPOSE": "0"})):
+            fn = os.path.join(td, f"{tag}.pt")
+            subprocess.run([sys.executable, "-c", code, fn], cwd=root,
+                           env=dict(os.environ, **env_add), check=True)
+            outs.append(torch_load(fn))
+    (a1, a2), (b1, b2) = outs
+    assert rel_l2(a1.numpy(), b1.numpy()) <= 1e-6
+    assert rel_l2(a2.numpy(), b2.numpy()) <= 1e-6
+    assert rel_l2(a2.numpy(), b1.numpy()[7:16]) <= 1e-6
+
+
 def torch_load(path):
     import torch
     return torch.load(path)

@@ -22,6 +22,13 @@
     python tools/bench_scale.py c5 [n=4096] [views=32] [slab=256]
     python tools/bench_scale.py ooc [n=2048] [views=64] [budget_gib=12]
     python tools/bench_scale.py c4 [n=1024] [views=1024] [iters=2] [block=32]
+    python tools/bench_scale.py oocloops [n=1536] [views=64] [budget_gib=6] [iters=3]
+
+* ``oocloops``: BASELINE config 5's mechanism (a volume larger than the device
+  budget reconstructed through slab streaming) with the loops themselves:
+  CGLS and SART-TV on host float32 vectors with every operator pass planned
+  and slab-streamed under a forced device budget, against the same loops
+  in-core on the device (the volume fits a B200's HBM, so both run here).
 
 Prints one JSON line per measurement.
 """
@@ -276,6 +283,66 @@ def c4(n=1024, A=1024, iters=2, block=32):
     print(json.dumps(out), flush=True)
 
 
+def oocloops(n=1536, A=64, budget_gib=6.0, iters=3):
+    """Out-of-core CGLS / SART-TV (forced budget) vs in-core on one GPU."""
+    import numpy as np
+    g = bench.make_geometry(n, A, cs)
+    dev = torch.device("cuda", 0)
+    x_true = cs.phantom(cs.PhantomKind.SHEPP_LOGAN_3D, g.voxel_grid,
+                        device=dev).data
+    b_d = cs.forward_project_slab(cs.Volume(g.voxel_grid, x_true), g, (0, A),
+                                  cs.ProjectionMethod.INTERPOLATED).data
+    del x_true
+    b_h = b_d.cpu().numpy()
+    del b_d
+    torch.cuda.empty_cache()
+    big = cs.DevicePool.b200(1)
+    small = cs.DevicePool((cs.DeviceSpec(
+        memory_budget=int(budget_gib * 2 ** 30), cuda_device=0),))
+    fplan, bplan = cs.plan_forward(g, small), cs.plan_backward(g, small)
+    tv = cs.TvParams(cs.TvMinimizer.GRADIENT_DESCENT, 1, 8, 1e-3)
+    out = {"measure": "ooc_loops", "n": n, "views": A, "iters": iters,
+           "budget_gib": budget_gib, "volume_gib": n ** 3 * 4 / 2 ** 30,
+           "fwd_splits": fplan.n_splits, "bwd_splits": bplan.n_splits}
+
+    def rel(a, b):
+        num = den = 0.0
+        for z in range(0, b.shape[0], 64):
+            d = a[z:z + 64].astype(np.float64) - b[z:z + 64]
+            num += float((d * d).sum())
+            den += float((b[z:z + 64].astype(np.float64) ** 2).sum())
+        return (num / den) ** 0.5
+
+    stack = cs.ProjectionStack(g.detector, b_h)
+    for name, run in (
+            ("cgls", lambda pool: cs.cgls(stack, g, cs.ReconConfig(
+                pool, cs.Algorithm.CGLS, iters))),
+            ("sart_tv", lambda pool: cs.os_sart(stack, g, cs.ReconConfig(
+                pool, cs.Algorithm.OSSART, iters, 16, tv=tv)))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r_in = run(big)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        x_in = np.asarray((r_in.volume if name == "cgls" else r_in).data)
+        res_in = list(r_in.residuals) if name == "cgls" else None
+        del r_in
+        torch.cuda.empty_cache()
+        t2 = time.perf_counter()
+        r_out = run(small)
+        t3 = time.perf_counter()
+        x_out = np.asarray((r_out.volume if name == "cgls" else r_out).data)
+        ent = {"in_core_s": t1 - t0, "out_of_core_s": t3 - t2,
+               "rel_l2_vs_in_core": rel(x_out, x_in)}
+        if name == "cgls":
+            ent["residuals_in"] = res_in
+            ent["residuals_out"] = list(r_out.residuals)
+        out[name] = ent
+        del r_out, x_in, x_out
+        torch.cuda.empty_cache()
+    print(json.dumps(out), flush=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1]
     args = [float(a) for a in sys.argv[2:]]
@@ -285,5 +352,8 @@ if __name__ == "__main__":
         c5(*[int(a) for a in args])
     elif what == "c4":
         c4(*[int(a) for a in args])
+    elif what == "oocloops":
+        oocloops(*([int(a) for a in args[:2]] + args[2:3] +
+                   [int(a) for a in args[3:4]]))
     else:
         ooc(*([int(args[0])] if args else []) + ([int(args[1])] if len(args) > 1 else []) + (args[2:3]))
