@@ -851,14 +851,29 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   // at 1024^3, +10% at 2048^3: the smaller boxes take more half-depth chunks
   // and flushes, which cost more once the slab is far beyond L2).  5 CTAs
   // (48 registers) spill.
-  // r02: with the matched boxes' T pitch padded to 32 words (below), 3 CTAs
-  // x 72 KB win at every size (512^3: 208.6 vs 201.3 GUPS dense for the
-  // unpadded 4 x 54 KB; 1024^3: 217.0 vs 210.2; profiles/ab_matched_tpad_r02t
-  // .jsonl)
   static const char* tp_env = getenv("CS_ST_TPAD");
   const bool padded = OP == OP_BWD && !(tp_env && atoi(tp_env) == 0);
-  const bool four = !padded &&
-                    (double)(z_hi - z_lo) * nx * ny <= 134217728.0;  // 512^3
+  // Matched, x-major views: run as y-major views of the transposed frame
+  // when the device has room for a slab-sized accumulator (see the launch
+  // below; knob CS_ST_TRANSPOSE=0 disables).
+  bool use_t = false;
+  const size_t slab_bytes = (size_t)(z_hi - z_lo) * nx * ny * sizeof(float);
+  if (OP == OP_BWD && nxm > 0) {
+    static const char* tk = getenv("CS_ST_TRANSPOSE");
+    size_t free_b = 0, total_b = 0;
+    use_t = !(tk && tk[0] == '0') &&
+            cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
+            free_b > slab_bytes + ((size_t)4 << 30);
+  }
+  // Occupancy: with every matched view y-major (transposed frame) 4 CTAs x
+  // 54 KB win (512^3: 250.6 vs 243.2 GUPS dense for 3 x 72 KB; 1024^3: 261.9
+  // vs 254.4; profiles/ab_matched_occupancy_r02ad.jsonl); x-major boxes in
+  // their own frame (y rows padded to 32 words) need 3 x 72 KB.
+  static const char* four_knob = getenv("CS_ST_FOUR");  // A/B: 4 CTAs/SM
+  const bool four =
+      four_knob ? four_knob[0] == '1'
+                : (padded ? (use_t || nxm == 0)
+                          : (double)(z_hi - z_lo) * nx * ny <= 134217728.0);
   static const char* kb_knob = getenv("CS_STAGED_SMEM_KB");
   // (3 CTAs: 72 KB boxes, +1-3% over 64 KB at 1024^3 / 2048^3; 80 KB no
   // longer fits three)
@@ -991,13 +1006,8 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   // 512^3 (profiles/ncu_r02w.md).  Needs a slab-sized buffer: used when the
   // device has room for it (knob CS_ST_TRANSPOSE=0 disables).
   bool transposed = false;
-  if (OP == OP_BWD && nxm > 0 && rows(0) > 0) {
-    static const char* tk = getenv("CS_ST_TRANSPOSE");
-    const size_t slab_bytes = (size_t)(z_hi - z_lo) * nx * ny * sizeof(float);
-    size_t free_b = 0, total_b = 0;
-    if (!(tk && tk[0] == '0') &&
-        cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
-        free_b > 2 * slab_bytes + ((size_t)2 << 30)) {
+  if (use_t && rows(0) > 0) {
+    {
       double* geom_t = (double*)malloc(sizeof(double) * 12 * (size_t)n_a);
       memcpy(geom_t, geom, sizeof(double) * 12 * (size_t)n_a);
       for (int a = 0; a < n_a; a++)
