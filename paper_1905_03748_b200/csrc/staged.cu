@@ -45,6 +45,7 @@ constexpr int ST_THREADS = ST_TU * ST_TV;
 #define CS_ST_ACC 0
 #endif
 constexpr int ST_S = CS_ST_S;  // planes per chunk along the main axis
+constexpr int ST_S_DEEP = 14;  // matched on large planes (launch_staged)
 
 
 // Float -> int without the conversion pipe: for |x| < 2^22, x + 1.5 * 2^23
@@ -109,7 +110,7 @@ __device__ __forceinline__ void st_red4(float* p, float a, float b, float c,
 // MINB = CTAs per SM: 3 (72 registers, 72 KB boxes) or 4 (64 registers, 54 KB
 // boxes; 4 x 54 KB + the static arrays fit an SM's 228 KB), chosen per launch
 // by the slab size (launch_staged).
-template <int OP, int M, int MODE, int MINB = 3>
+template <int OP, int M, int MODE, int MINB = 3, int SD = ST_S>
 __global__ void __launch_bounds__(ST_THREADS, MINB)
     staged_kernel(const float* __restrict__ vol_in, float* __restrict__ vol_acc,
                   const AngleGeom* __restrict__ geom,
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
     if (has) {
 #pragma unroll
       for (int ci = 0; ci < 2; ci++) {
-        const int S = ST_S >> ci;
+        const int S = SD >> ci;
         const int c_lo = dir > 0 ? cur : cur - S + 1;
         const int c_hi = c_lo + S - 1;
         // last sample of the chunk: qM(k) crosses the far face at
@@ -371,15 +372,15 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
     };
     bool prec = false;
     if (OP == OP_BWD) {
-      const float c0f = (float)(dir > 0 ? cur : cur - ST_S + 1);
+      const float c0f = (float)(dir > 0 ? cur : cur - SD + 1);
       const float sq_m = s_sqm;
       prec = s_pall ||
-             s_gap * fmaxf(fabsf(c0f - sq_m), fabsf(c0f + ST_S - sq_m)) >=
+             s_gap * fmaxf(fabsf(c0f - sq_m), fabsf(c0f + SD - sq_m)) >=
                  prec_fp;
     }
     const int cap_eff = prec ? box_cap / 2 : box_cap;  // int2 entries
-    const int ci = (ext8[0] > ext8[1] || box_size(0, ST_S) <= cap_eff) ? 0 : 1;
-    const int S = ST_S >> ci;
+    const int ci = (ext8[0] > ext8[1] || box_size(0, SD) <= cap_eff) ? 0 : 1;
+    const int S = SD >> ci;
     const int c_lo = dir > 0 ? cur : cur - S + 1;
     cur += dir * S;
     const int ka = k;
@@ -870,15 +871,15 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   // vs 254.4; profiles/ab_matched_occupancy_r02ad.jsonl); x-major boxes in
   // their own frame (y rows padded to 32 words) need 3 x 72 KB.
   static const char* four_knob = getenv("CS_ST_FOUR");  // A/B: 4 CTAs/SM
-  const bool four =
+  bool four =
       four_knob ? four_knob[0] == '1'
                 : (padded ? (use_t || nxm == 0)
                           : (double)(z_hi - z_lo) * nx * ny <= 134217728.0);
   static const char* kb_knob = getenv("CS_STAGED_SMEM_KB");
   // (3 CTAs: 72 KB boxes, +1-3% over 64 KB at 1024^3 / 2048^3; 80 KB no
   // longer fits three)
-  const size_t smem = (kb_knob ? (size_t)atoi(kb_knob) : four ? 54 : 72) * 1024;
-  const int cap = (int)(smem / sizeof(float));
+  size_t smem = (kb_knob ? (size_t)atoi(kb_knob) : four ? 54 : 72) * 1024;
+  int cap = (int)(smem / sizeof(float));
   double taps = 1.0;
   const float budget =
       OP == OP_BWD ? fixed_point_budget(grid6, nx, ny, nz, geom, n_a, n_u, n_v,
@@ -980,8 +981,24 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     const int rv = ST_TV / lane_stride;
     return (unsigned)((band[c][1] - band[c][0] + rv - 1) / rv);
   };
-  auto k0 = four ? staged_kernel<OP, 0, MODE, 4> : staged_kernel<OP, 0, MODE, 3>;
-  auto k1 = four ? staged_kernel<OP, 1, MODE, 4> : staged_kernel<OP, 1, MODE, 3>;
+  // matched chunk depth: 14 planes with 3 CTAs x 72 KB boxes for planes of
+  // >= 512^2 voxels (512^3: 261.6 vs 249.1 GUPS dense for 8 planes at 4 x 54
+  // KB, 1024^3: 271.6 vs 262.1, 2048^3 x 32 views: 260.5 vs 263.9), else 8
+  // (256^3: 165 vs 189; profiles/ab_matched_depth_r02ai.jsonl)
+  static const char* deep_knob = getenv("CS_ST_DEEP");  // A/B: 0 / 1
+  const bool deep =
+      OP == OP_BWD && padded && !(four_knob || kb_knob) &&
+      (deep_knob ? deep_knob[0] == '1'
+                 : (use_t || nxm == 0) && (double)nx * ny >= 262144.0);
+  if (deep) {
+    four = false;
+    smem = 72 * 1024;
+    cap = (int)(smem / sizeof(float));
+  }
+  auto k0 = deep ? staged_kernel<OP, 0, MODE, 3, ST_S_DEEP>
+            : four ? staged_kernel<OP, 0, MODE, 4> : staged_kernel<OP, 0, MODE, 3>;
+  auto k1 = deep ? staged_kernel<OP, 1, MODE, 3, ST_S_DEEP>
+            : four ? staged_kernel<OP, 1, MODE, 4> : staged_kernel<OP, 1, MODE, 3>;
   // the dynamic shared-memory opt-in is per device: set it once on each
   // (the executor drives several GPUs from one process)
   static std::atomic<unsigned long long> attr_done{0};
@@ -990,7 +1007,9 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   const unsigned long long bit = 1ull << (dev_ord & 63);
   if (!(attr_done.load() & bit)) {
     for (auto k : {staged_kernel<OP, 0, MODE, 3>, staged_kernel<OP, 1, MODE, 3>,
-                   staged_kernel<OP, 0, MODE, 4>, staged_kernel<OP, 1, MODE, 4>})
+                   staged_kernel<OP, 0, MODE, 4>, staged_kernel<OP, 1, MODE, 4>,
+                   staged_kernel<OP, 0, MODE, 3, ST_S_DEEP>,
+                   staged_kernel<OP, 1, MODE, 3, ST_S_DEEP>})
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            200 * 1024);
     attr_done.fetch_or(bit);
