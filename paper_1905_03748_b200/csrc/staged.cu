@@ -44,6 +44,12 @@ constexpr int ST_THREADS = ST_TU * ST_TV;
 #ifndef CS_ST_ACC
 #define CS_ST_ACC 0
 #endif
+// matched: zero the box words as the flush reads them (one zeroing of the
+// whole box per CTA instead of one pass per chunk: 512^3 dense 259.8 -> 265.9
+// GUPS, 256^3 188.7 -> 207.9; profiles/ab_matched_zof_r02am.jsonl)
+#ifndef CS_ST_ZOF
+#define CS_ST_ZOF 1
+#endif
 constexpr int ST_S = CS_ST_S;  // planes per chunk along the main axis
 constexpr int ST_S_DEEP = 14;  // matched on large planes (launch_staged)
 
@@ -310,6 +316,9 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
   // Chunks of ST_S cells along M in march order; a chunk whose box would
   // not fit the shared budget is retried at ST_S / 2 cells (both candidate
   // extents are reduced in one pass), and only then served from global.
+  if (OP == OP_BWD && CS_ST_ZOF) {  // the flushes keep it zero afterwards
+    for (int i = threadIdx.x; i < box_cap; i += ST_THREADS) box_i[i] = 0;
+  }
   int k = k0;
   int cur = dir > 0 ? mlo : mhi;  // next M-cell in march order
   // reciprocal of the M step for the chunk-end estimates (an estimate:
@@ -474,11 +483,11 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
             st_box[d + 3 * sx] = q4.w;
           }
         }
-      } else {
+      } else if (!CS_ST_ZOF) {
         const int nw = prec ? 2 * bsize : bsize;
         for (int i = threadIdx.x; i < nw; i += ST_THREADS) box_i[i] = 0;
       }
-      __syncthreads();
+      if (OP == OP_FWD || !CS_ST_ZOF) __syncthreads();
     }
     // ---- samples of the chunk: one instantiation of the march per box
     // mode (MODE_BOX: one-word box / Ax box reads, MODE_PREC: two-word
@@ -637,7 +646,11 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
       const int pstride = fold ? P : ST_THREADS;
       const int bz0 = max(0, z_lo - bo[2]), bz1 = min(bn[2], z_hi - bo[2]);
       int bzs = z_first;
-      while (bzs < bz0) bzs += zstep;
+      // zero-on-flush: every plane and row of the box is read (and zeroed);
+      // only those inside the grid and slab are reduced into the volume
+      if (!CS_ST_ZOF)
+        while (bzs < bz0) bzs += zstep;
+      const int bze = CS_ST_ZOF ? bn[2] : bz1;
       const float il = inv_scale / lo_scale;
       const int wps = prec ? 2 : 1;                // words per box voxel
       const int bstep = zstep * sz * wps;
@@ -653,14 +666,16 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
           by = cp - xq * bn[1];
         }
         const int gx = bo[0] + 4 * xq, gy = bo[1] + by;
-        if (gy < 0 || gy >= ny) continue;
+        const bool row_in = gy >= 0 && gy < ny;
+        if (!CS_ST_ZOF && !row_in) continue;
         const bool vec = vec_ok && gx >= 0 && gx + 3 < nx;
         const int* bp = box_i + (by * sy + 4 * xq * sx + bzs * sz) * wps;
         float* gp = vol_acc + (size_t)(bo[2] + bzs - z_lo) * plane +
                     (size_t)gy * nx + gx;
         const int sxw = sx * wps;
-        for (int bz = bzs; bz < bz1; bz += zstep, bp += bstep, gp += gstep) {
+        for (int bz = bzs; bz < bze; bz += zstep, bp += bstep, gp += gstep) {
           float f0, f1, f2, f3;
+          int* bw = const_cast<int*>(bp);
           if (prec) {
             int2 q0, q1, q2, q3;
             if (M == 1) {
@@ -676,6 +691,16 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
             }
             if ((q0.x | q0.y | q1.x | q1.y | q2.x | q2.y | q3.x | q3.y) == 0)
               continue;
+            if (CS_ST_ZOF) {
+              if (M == 1) {
+                *reinterpret_cast<int4*>(bw) = make_int4(0, 0, 0, 0);
+                *reinterpret_cast<int4*>(bw + 4) = make_int4(0, 0, 0, 0);
+              } else {
+                for (int j = 0; j < 4; j++)
+                  *reinterpret_cast<int2*>(bw + j * sxw) = make_int2(0, 0);
+              }
+              if (!row_in || bz < bz0 || bz >= bz1) continue;
+            }
             f0 = fmaf((float)q0.y, il, (float)q0.x * inv_scale);
             f1 = fmaf((float)q1.y, il, (float)q1.x * inv_scale);
             f2 = fmaf((float)q2.y, il, (float)q2.x * inv_scale);
@@ -692,6 +717,14 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
               q3 = bp[3 * sxw];
             }
             if ((q0 | q1 | q2 | q3) == 0) continue;
+            if (CS_ST_ZOF) {
+              if (M == 1) {
+                *reinterpret_cast<int4*>(bw) = make_int4(0, 0, 0, 0);
+              } else {
+                for (int j = 0; j < 4; j++) bw[j * sxw] = 0;
+              }
+              if (!row_in || bz < bz0 || bz >= bz1) continue;
+            }
             f0 = (float)q0 * inv_scale; f1 = (float)q1 * inv_scale;
             f2 = (float)q2 * inv_scale; f3 = (float)q3 * inv_scale;
           }
