@@ -65,6 +65,15 @@ __device__ __forceinline__ int magic_int(float biased) {
   return __float_as_int(biased) - 0x4B400000;
 }
 
+// a / b for 0 <= a < 2^22, 0 < b < 2^22 without the integer-division
+// sequence (~25 instructions): fp32 reciprocal estimate, one correction
+__device__ __forceinline__ int small_div(int a, int b, float rb) {
+  int q = (int)((float)a * rb);
+  const int r = a - q * b;
+  q += r >= b ? 1 : (r < 0 ? -1 : 0);
+  return q;
+}
+
 __device__ __forceinline__ int qfloor(const March& m, int k, int axis) {
   return q_cell(q_at(m, k, axis));  // exact (common.cuh)
 }
@@ -641,8 +650,9 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
       const int qpr_ = bn[0] >> 2;
       const int P = qpr_ * bn[1];                  // columns per z-plane
       const bool fold = P <= ST_THREADS;           // several z per pass
-      const int zstep = fold ? ST_THREADS / P : 1;
-      const int z_first = fold ? threadIdx.x / P : 0;
+      const float rP = 1.f / (float)P;
+      const int zstep = fold ? small_div(ST_THREADS, P, rP) : 1;
+      const int z_first = fold ? small_div(threadIdx.x, P, rP) : 0;
       const int pstride = fold ? P : ST_THREADS;
       const int bz0 = max(0, z_lo - bo[2]), bz1 = min(bn[2], z_hi - bo[2]);
       int bzs = z_first;
@@ -655,14 +665,15 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
       const int wps = prec ? 2 : 1;                // words per box voxel
       const int bstep = zstep * sz * wps;
       const size_t gstep = (size_t)zstep * plane;
+      const float rq = 1.f / (float)(M == 1 ? qpr_ : bn[1]);
       for (int cp = fold ? threadIdx.x - z_first * P : threadIdx.x;
            z_first < zstep && cp < P; cp += pstride) {
         int xq, by;
         if (M == 1) {
-          by = cp / qpr_;
+          by = small_div(cp, qpr_, rq);
           xq = cp - by * qpr_;
         } else {
-          xq = cp / bn[1];
+          xq = small_div(cp, bn[1], rq);
           by = cp - xq * bn[1];
         }
         const int gx = bo[0] + 4 * xq, gy = bo[1] + by;
