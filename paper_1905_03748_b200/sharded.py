@@ -371,7 +371,8 @@ def os_sart_sharded(b_local: torch.Tensor, ops: ShardedOperators, blocks,
     blocks in order, see block_rows).  W_S / V_S are the guarded inverses of
     A_S 1 / A_S^T 1; the V_S of all blocks are kept while they fit
     ``weight_budget`` bytes, else recomputed per block (one more A^T per
-    block and iteration instead of n_blocks slab-sized buffers).  ``tv``
+    block and iteration for the blocks beyond the budget, instead of
+    n_blocks slab-sized buffers).  ``tv``
     (TvParams) runs the halo-exchanged TV step after every iteration
     (``tv_step(x) -> x`` replaces it, e.g. the single-GPU split_minimize)."""
     rows, n_local = block_rows(blocks, ops.world, ops.rank)
@@ -382,7 +383,8 @@ def os_sart_sharded(b_local: torch.Tensor, ops: ShardedOperators, blocks,
     slab_bytes = 4 * shape[1] * shape[2] * max(z1 - z0 for z0, z1 in ops.slabs)
     if weight_budget is None:
         weight_budget = 1 << 62
-    keep_v = slab_bytes * len(blocks) <= weight_budget
+    # as many blocks' V_S as fit are kept, the rest recomputed per block
+    n_keep = min(len(blocks), int(weight_budget // max(slab_bytes, 1)))
     ones_slab = torch.ones(shape, dtype=torch.float32, device=b_local.device)
     w_all = torch.empty_like(b_local)
 
@@ -398,8 +400,7 @@ def os_sart_sharded(b_local: torch.Tensor, ops: ShardedOperators, blocks,
         w = w_all[off:off + s1 - s0]
         ops.forward(ones_slab, w, (b0, b1))
         vec.guarded_inverse(w)
-        if keep_v:
-            vs.append(col_inverse(b0, b1, s0, s1))
+        vs.append(col_inverse(b0, b1, s0, s1) if len(vs) < n_keep else None)
     del ones_slab
     x = _zeros(shape, b_local)
     upd = torch.zeros_like(x)
@@ -417,7 +418,7 @@ def os_sart_sharded(b_local: torch.Tensor, ops: ShardedOperators, blocks,
                 vec.weighted_residual(res, b_local[off:off + s1 - s0],
                                       w_all[off:off + s1 - s0])
             ops.backward(res, upd, (b0, b1))
-            v = vs[i] if keep_v else col_inverse(b0, b1, s0, s1)
+            v = vs[i] if vs[i] is not None else col_inverse(b0, b1, s0, s1)
             vec.sart_update(x, upd, v, relaxation)
         if tv_step is not None:
             x = tv_step(x)

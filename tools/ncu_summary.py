@@ -41,6 +41,7 @@ KEYS = {"fwd_mlayer": "fwd_mlayer_kernel", "fill_xlayers": "fwd_mlayer_kernel",
         "fill_ylayers": "fwd_mlayer_kernel",
         "fwd_interp": "fwd_interp_kernel",
         "staged_kernel<1": "bwd_matched_kernel",
+        "transpose_add": "bwd_matched_kernel",
         "bwd_fdk": "bwd_fdk_kernel", "fdk_staged": "bwd_fdk_kernel",
         "fwd_siddon": "fwd_siddon_kernel",
         "tv_march2_kernel<1": "tv_gd_fused_kernel",
@@ -97,7 +98,8 @@ def main():
         limits = {}
     for rec in rows_out:
         for k, key in KEYS.items():
-            if k not in rec["kernel"] or k.startswith("fill_"):
+            if (k not in rec["kernel"] or k.startswith("fill_")
+                    or k == "transpose_add"):
                 continue
             ent = {}
             for label in ("TEX writeback %", "issue active %", "L1/TEX thru %",
