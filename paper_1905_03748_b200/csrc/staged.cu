@@ -155,7 +155,10 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
     atomicAdd(p + 1, magic_int(fmaf(e, lo_scale, ST_MAGIC)));
   };
   __shared__ int ext[8];   // mlo, mhi, -, -, -, -, dir flags
-  __shared__ int ext8[8];  // per chunk candidate: tlo, thi, zlo, zhi (x2)
+  // per chunk candidate: tlo, thi, zlo, zhi (x2); double-buffered by chunk
+  // parity, so the next chunk's set is reset while this one is read (two
+  // barriers per chunk instead of three)
+  __shared__ int ext8s[2][8];
   __shared__ float s_scale;
   __shared__ float s_gap;  // largest neighbouring-ray slope difference
   __shared__ float s_sqm;  // the source's q coordinate along M
@@ -328,6 +331,10 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
   if (OP == OP_BWD && CS_ST_ZOF) {  // the flushes keep it zero afterwards
     for (int i = threadIdx.x; i < box_cap; i += ST_THREADS) box_i[i] = 0;
   }
+  if (threadIdx.x < 16)
+    ext8s[threadIdx.x >> 3][threadIdx.x & 7] =
+        (threadIdx.x & 1) ? INT_MIN : INT_MAX;
+  int par = 0;
   int k = k0;
   int cur = dir > 0 ? mlo : mhi;  // next M-cell in march order
   // reciprocal of the M step for the chunk-end estimates (an estimate:
@@ -335,45 +342,47 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
   const float rbm = has ? 1.f / m.B[M] : 0.f;
   const bool run = !mixed;
   while (run && (dir > 0 ? cur <= mhi : cur >= mlo)) {
-    // candidate chunks: S = ST_S (index 0) and ST_S / 2 (index 1)
+    // candidate chunks: S = SD (index 0) and, only when its box does not
+    // fit the shared budget (a CTA-uniform decision), SD / 2 (index 1)
     int kbc[2] = {k, k};
-    if (has) {
-#pragma unroll
-      for (int ci = 0; ci < 2; ci++) {
-        const int S = SD >> ci;
-        const int c_lo = dir > 0 ? cur : cur - S + 1;
-        const int c_hi = c_lo + S - 1;
-        // last sample of the chunk: qM(k) crosses the far face at
-        // k* = kc + (face - A_M) / B_M; estimate, then settle on the exact
-        // fp32 cell test (the same floor the sampling loop uses)
-        const float face = dir > 0 ? (float)(c_hi + 1) : (float)c_lo;
-        const float kst = (face - m.A[M]) * rbm + (float)(int)m.kc;
-        int ke = (int)fminf(fmaxf(ceilf(kst), (float)k), (float)k1);
-        if (dir > 0) {
-          while (ke > k && qfloor(m, ke - 1, M) > c_hi) ke--;
-          while (ke < k1 && qfloor(m, ke, M) <= c_hi) ke++;
-        } else {
-          while (ke > k && qfloor(m, ke - 1, M) < c_lo) ke--;
-          while (ke < k1 && qfloor(m, ke, M) >= c_lo) ke++;
-        }
-        kbc[ci] = ke;
+    // last sample of candidate ci: qM(k) crosses the far face at
+    // k* = kc + (face - A_M) / B_M; estimate, then settle on the exact cell
+    // test (the same floor the sampling loop uses)
+    auto chunk_end = [&](int ci) {
+      const int S = SD >> ci;
+      const int c_lo = dir > 0 ? cur : cur - S + 1;
+      const int c_hi = c_lo + S - 1;
+      const float face = dir > 0 ? (float)(c_hi + 1) : (float)c_lo;
+      const float kst = (face - m.A[M]) * rbm + (float)(int)m.kc;
+      int ke = (int)fminf(fmaxf(ceilf(kst), (float)k), (float)k1);
+      if (dir > 0) {
+        while (ke > k && qfloor(m, ke - 1, M) > c_hi) ke--;
+        while (ke < k1 && qfloor(m, ke, M) <= c_hi) ke++;
+      } else {
+        while (ke > k && qfloor(m, ke - 1, M) < c_lo) ke--;
+        while (ke < k1 && qfloor(m, ke, M) >= c_lo) ke++;
       }
-    }
-    __syncthreads();  // previous chunk's box fully consumed
-    if (threadIdx.x < 8) ext8[threadIdx.x] = (threadIdx.x & 1) ? INT_MIN : INT_MAX;
-    __syncthreads();
-#pragma unroll
-    for (int ci = 0; ci < 2; ci++) {
+      return ke;
+    };
+    // this ray's T / z extent over samples [k, ke) into candidate ci's slots
+    auto extents = [&](int* e8, int ci) {
       if (kbc[ci] > k) {
         const int t0 = qfloor(m, k, T), t1 = qfloor(m, kbc[ci] - 1, T);
         const int zz0 = qfloor(m, k, 2), zz1 = qfloor(m, kbc[ci] - 1, 2);
-        atomicMin(&ext8[4 * ci + 0], min(t0, t1));
-        atomicMax(&ext8[4 * ci + 1], max(t0, t1));
-        atomicMin(&ext8[4 * ci + 2], min(zz0, zz1));
-        atomicMax(&ext8[4 * ci + 3], max(zz0, zz1));
+        atomicMin(&e8[4 * ci + 0], min(t0, t1));
+        atomicMax(&e8[4 * ci + 1], max(t0, t1));
+        atomicMin(&e8[4 * ci + 2], min(zz0, zz1));
+        atomicMax(&e8[4 * ci + 3], max(zz0, zz1));
       }
-    }
+    };
+    if (has) kbc[0] = chunk_end(0);
+    __syncthreads();  // previous chunk's box consumed; ext8 reset
+    int* ext8 = ext8s[par];
+    extents(ext8, 0);
     __syncthreads();
+    if (threadIdx.x < 8)  // the next chunk's set (read after its barrier)
+      ext8s[par ^ 1][threadIdx.x] = (threadIdx.x & 1) ? INT_MIN : INT_MAX;
+    par ^= 1;
     // box size for a candidate (same formula as the layout below)
     auto box_size = [&](int ci, int S) {
       const int c_lo = dir > 0 ? cur : cur - S + 1;
@@ -398,6 +407,11 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
     }
     const int cap_eff = prec ? box_cap / 2 : box_cap;  // int2 entries
     const int ci = (ext8[0] > ext8[1] || box_size(0, SD) <= cap_eff) ? 0 : 1;
+    if (ci) {  // CTA-uniform: the half-depth candidate, reduced now
+      if (has) kbc[1] = chunk_end(1);
+      extents(ext8, 1);
+      __syncthreads();
+    }
     const int S = SD >> ci;
     const int c_lo = dir > 0 ? cur : cur - S + 1;
     cur += dir * S;
