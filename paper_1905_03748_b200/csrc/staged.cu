@@ -47,6 +47,13 @@ constexpr int ST_THREADS = ST_TU * ST_TV;
 // matched: zero the box words as the flush reads them (one zeroing of the
 // whole box per CTA instead of one pass per chunk: 512^3 dense 259.8 -> 265.9
 // GUPS, 256^3 188.7 -> 207.9; profiles/ab_matched_zof_r02am.jsonl)
+// matched: launch order with the view index fastest (CTAs of neighbouring
+// views of one detector tile run together, so their box flushes hit L2):
+// 2048^3 x 32 views 262.5 -> 273.8 GUPS dense, 1024^3 265.0 -> 268.9, 512^3
+// neutral (profiles/ab_matched_viewfast_r02ar.jsonl)
+#ifndef CS_ST_VIEWFAST
+#define CS_ST_VIEWFAST 1
+#endif
 #ifndef CS_ST_ZOF
 #define CS_ST_ZOF 1
 #endif
@@ -169,11 +176,15 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
   // 8 / s rows and a warp's lanes are s pixels apart, so with pixels finer
   // than voxels the lanes of one ATOMS instruction seldom hit the same
   // shared word (same-address atomics serialise)
-  const int u = blockIdx.x * (ST_TU * lane_stride) + lane * lane_stride +
+  const bool vf = OP == OP_BWD && CS_ST_VIEWFAST;
+  const int bidx = vf ? blockIdx.y : blockIdx.x;   // detector u tile
+  const int bidy = vf ? blockIdx.z : blockIdx.y;   // detector v tile
+  const int bidv = vf ? blockIdx.x : blockIdx.z;   // view
+  const int u = bidx * (ST_TU * lane_stride) + lane * lane_stride +
                 (warp & (lane_stride - 1));
-  const int v = v_base + blockIdx.y * (ST_TV / lane_stride) +
+  const int v = v_base + bidy * (ST_TV / lane_stride) +
                 warp / lane_stride;
-  const int a = view_ids[blockIdx.z];
+  const int a = view_ids[bidv];
   const bool valid = u < n_u && v < v_end;
   const int nx = G.n[0], ny = G.n[1];
   const size_t plane = (size_t)nx * ny;
@@ -279,7 +290,7 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
     bool pc = prec_mode == 1;
     if (prec_mode == 0) {
       const int tu = ST_TU * lane_stride, tv = ST_TV / lane_stride;
-      const int u_first = blockIdx.x * tu, v_first = v_base + blockIdx.y * tv;
+      const int u_first = bidx * tu, v_first = v_base + bidy * tv;
       pc = u_first < edge || u_first + tu > n_u - edge ||
            v_first < edge || v_first + tv > n_v - edge;
       const AngleGeom& ag = geom[a];
@@ -1053,6 +1064,9 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     smem = 72 * 1024;
     cap = (int)(smem / sizeof(float));
   }
+  auto grid_of = [&](unsigned tu, unsigned tv, unsigned nv) {
+    return (OP == OP_BWD && CS_ST_VIEWFAST) ? dim3(nv, tu, tv) : dim3(tu, tv, nv);
+  };
   auto k0 = deep ? staged_kernel<OP, 0, MODE, 3, ST_S_DEEP>
             : four ? staged_kernel<OP, 0, MODE, 4> : staged_kernel<OP, 0, MODE, 3>;
   auto k1 = deep ? staged_kernel<OP, 1, MODE, 3, ST_S_DEEP>
@@ -1107,7 +1121,7 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
         e2 = cudaMemsetAsync(acc_t, 0, slab_bytes, s);
       if (!rc && e2 == cudaSuccess) {
         const int vec_t = (ny % 4 == 0);
-        k1<<<dim3(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
+        k1<<<grid_of(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
             vol_in, acc_t, dgeom_t, ids, GT, step_max, z_lo, z_hi, n_u, n_v,
             band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_t,
             lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad);
@@ -1135,14 +1149,14 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     }
   }
   if (!transposed && nxm > 0 && rows(0) > 0) {
-    k0<<<dim3(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
+    k0<<<grid_of(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids, G, step_max, z_lo, z_hi, n_u, n_v,
         band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_ok,
         lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad);
     CS_COUNT_LAUNCH();
   }
   if (nall > nxm && rows(1) > 0) {
-    k1<<<dim3(gx, rows(1), nall - nxm), ST_THREADS, smem, s>>>(
+    k1<<<grid_of(gx, rows(1), nall - nxm), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids + nxm, G, step_max, z_lo, z_hi, n_u, n_v,
         band[1][0], band[1][1], out, proj_in, rb, rw, cap, budget, vec_ok,
         lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad);
