@@ -655,7 +655,7 @@ def run_extras(args, cs, K, g, vol, y, dev):
     sparse = torch.empty_like(y)
     K.fwd_interp(vol, g, (0, A), (0, n), sparse)
     out["atb_matched_sparse_gups"] = upd / rate(
-        lambda: K.bwd_matched(sparse, g, (0, A), (0, n), acc), 1) / 1e9
+        lambda: K.bwd_matched(sparse, g, (0, A), (0, n), acc), 3) / 1e9
     del sparse
     # TV-GD iteration as the loops run it: in steady state one fused pass
     # per iteration (step i + gradient i+1 + Sigma g^2, tv.cu
