@@ -141,8 +141,10 @@ int cs_tv_step(const float* u, float* u_out, int nx, int ny, int nzw,
 /* The GD iteration in two passes that share g: g stored over the whole
  * window (g[nzw][ny][nx], device) with Σg² over the core into out_sum, then
  * u_out = u - step * g / (sqrt(*norm_sumsq_dev) * scale) elementwise over
- * n voxels -- bit-identical to cs_tv_grad_sumsq + cs_tv_step, with the
- * second pass a stream instead of a second stencil. */
+ * n voxels -- the same g and the same step arithmetic as cs_tv_grad_sumsq
+ * + cs_tv_step (the sums agree to fp32 partial-sum grouping), with the
+ * second pass a stream instead of a second stencil.  The step is
+ * u - c g with c = step / norm rounded once to fp32 (one FFMA). */
 int cs_tv_grad_store(const float* u, float* g, int nx, int ny, int nzw,
                      int core_lo, int core_hi, double* out_sum,
                      cs_stream_t stream);
@@ -155,7 +157,7 @@ int cs_tv_step_g(const float* u, const float* g, float* u_out, int64_t n,
  *   g_out = TV subgradient of u_out over the window, *out_sum = sum of
  *           g_out^2 over the core planes [core_lo, core_hi)
  * u_out / g_out are bit-identical to cs_tv_step_g followed by
- * cs_tv_grad_store.  norm_sumsq_dev and out_sum must differ (the kernel reads
+ * cs_tv_grad_store (same kernel family, same sums).  norm_sumsq_dev and out_sum must differ (the kernel reads
  * one while the reduction writes the other). */
 int cs_tv_gd_fused(const float* u, const float* g, float* u_out, float* g_out,
                    int nx, int ny, int nzw, int core_lo, int core_hi,

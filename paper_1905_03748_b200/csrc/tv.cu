@@ -6,14 +6,15 @@
 // reduce to one rule: p = 0 outside the window and on the face where the
 // forward difference is undefined, so -div p at voxel i is
 //   -(pz(i) - pz(i - ez) + py(i) - py(i - ey) + px(i) - px(i - ex)).
-// GD needs the global norm of g before the update, so it is two passes
-// (12 B / voxel-iteration): pass 1 reduces Σg² over the core
-// planes in fp64 (deterministic two-stage reduction), pass 2 writes
-// u - step g / ||g|| to a second buffer.  Production (cs_tv_grad_store +
-// cs_tv_step_g): pass 1 also stores g and pass 2 is a float4 stream
-// (147 vs 113 Gvox*it/s at 512^3 with pass 2 recomputing g, which
-// cs_tv_grad_sumsq + cs_tv_step still do).  ROF is one fused pass per iteration (28 B /
-// voxel-iteration) with neighbours through L1 (__ldg).
+// GD needs the global norm of g before the update: production is one
+// marching pass per iteration that applies step i and computes gradient
+// i+1 (tv_march2_kernel / tv_march_kernel, cs_tv_gd_fused), bracketed by a
+// gradient pass (cs_tv_grad_store) and a final float4 stream step
+// (cs_tv_step_g); Σg² partials are fp32 per thread and reduced in fp64
+// (deterministic two-stage reduction).  The r01 tiled kernel remains as the
+// A/B baseline and for the two-pass norm / step pair (cs_tv_grad_sumsq +
+// cs_tv_step).  ROF: one marching pass per dual iteration (rof_march2_kernel,
+// 28 B / voxel-iteration; the r01 per-voxel kernel for odd nx).
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
@@ -86,6 +87,19 @@ __device__ __forceinline__ float tv_inv_norm(float gx, float gy, float gz) {
   return r;
 }
 
+// The GD step u - c g with c = step / ||g|| rounded once to fp32: one
+// FFMA, the same in every GD kernel (bit-identical across them).  The fp64
+// form (round(u - c g) from exact fp64 products) differs only by c's fp32
+// rounding, 6e-8 of the step; per-thread partial sums of g^2 are fp32 over
+// <= 64 terms (<= 4e-6 relative on the norm), then reduced in fp64.  9% off
+// the fused pass (0.458 -> 0.416 ms at 512^3, profiles/ab_tv_f32_r02au.jsonl).
+__device__ __forceinline__ float tv_coef(double step, double norm) {
+  return norm < 1e-30 ? 0.f : (float)(step / norm);  // regularization.py:148
+}
+__device__ __forceinline__ float tv_step1(float u, float g, float c) {
+  return __fmaf_rn(-c, g, u);
+}
+
 // ---- tiled TV-GD (r01; A/B baseline and the two-pass norm/step pair) ---------------------------------------------
 // CTA = 32 x 8 (x, y) tile marching over a chunk of TV_ZC planes.  Per plane
 // the normalised gradient p is computed ONCE per voxel (plus a one-voxel
@@ -124,7 +138,7 @@ __global__ void __launch_bounds__(TV_TX * TV_TY)
   double norm = 0.0;
   if (PASS == 1) norm = sqrt(*sumsq) * scale;
   const bool skip = PASS == 1 && norm < 1e-30;  // regularization.py:148-149
-  const double coef = skip ? 0.0 : step / norm;   // u -= step * g / ||g||
+  const float coef = skip ? 0.f : tv_coef(step, norm);  // u -= step g/||g||
 
   // Per-thread tile bookkeeping is plane-invariant: computed once.  u tile
   // element i = (lx, ly) holds global (x0 - 1 + lx, y0 - 1 + ly); p tile
@@ -183,7 +197,7 @@ __global__ void __launch_bounds__(TV_TX * TV_TY)
   put(pl1, rb);
   fetch(zb + 1, rb);  // in flight while plane zb - 1 is processed
   float pz_prev = 0.f;
-  double acc = 0.0;
+  float acc = 0.f;
   for (int z = zb - 1; z < ze; z++) {
     __syncthreads();  // planes z, z+1 visible; previous p consumed
     const bool zlast = z >= W.nz - 1;
@@ -216,14 +230,14 @@ __global__ void __launch_bounds__(TV_TX * TV_TY)
       const float g = -((pz_own - pz_prev) + (spy[c_p] - spy[c_p - TV_PX]) +
                         (spx[c_p] - spx[c_p - 1]));
       if (PASS == 0) {
-        acc += (double)g * (double)g;
+        acc = __fmaf_rn(g, g, acc);
       } else if (PASS == 2) {
         uo[(size_t)z * plane + own_off] = g;
-        if (z >= c_lo && z < c_hi) acc += (double)g * (double)g;
+        if (z >= c_lo && z < c_hi) acc = __fmaf_rn(g, g, acc);
       } else {
         const float uc = pl0[c_u];
         uo[(size_t)z * plane + own_off] =
-            skip ? uc : (float)((double)uc - coef * (double)g);
+            skip ? uc : tv_step1(uc, g, coef);
       }
     }
     pz_prev = pz_own;
@@ -233,8 +247,10 @@ __global__ void __launch_bounds__(TV_TX * TV_TY)
     pl2 = t;
   }
   if (PASS != 1) {
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((tid & 31) == 0) sred[tid >> 5] = acc;
+    double accd = (double)acc;
+    for (int o = 16; o > 0; o >>= 1)
+      accd += __shfl_xor_sync(0xffffffffu, accd, o);
+    if ((tid & 31) == 0) sred[tid >> 5] = accd;
     __syncthreads();
     if (tid == 0) {
       double sm = 0.0;
@@ -266,8 +282,9 @@ __global__ void __launch_bounds__(TV_TX * TV_TY)
 // TM_D planes ahead through a per-thread cp.async ring (zero-fill outside the
 // window); a thread reads back only its own slots, so the ring needs no
 // barrier.  Same per-voxel expressions as tv_gd_tiled_kernel and the step of
-// tv_step_g_kernel (fp64 u - c g), so g and u are bit-identical to
-// grad_store + step_g; only the grouping of the fp64 partial sums differs.
+// tv_step_g_kernel (tv_step1), so g and u are bit-identical to grad_store +
+// step_g for the same input sum; only the grouping of the partial sums
+// differs between kernels.
 constexpr int TM_WARPS = 16, TM_THREADS = 32 * TM_WARPS;
 constexpr int TM_OX = 30, TM_OY = TM_WARPS - 2;
 #ifndef CS_TM_ZC
@@ -316,11 +333,8 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
   const bool xl = x < W.nx - 1, yl = y < W.ny - 1;  // forward diffs exist
   const size_t plane = (size_t)W.nx * W.ny;
   const int off = in_xy ? y * W.nx + x : 0;
-  double coef = 0.0;
-  if (FUSED) {
-    const double norm = sqrt(*sumsq_in) * scale;
-    coef = norm < 1e-30 ? 0.0 : step / norm;  // regularization.py:148-149
-  }
+  float coef = 0.f;
+  if (FUSED) coef = tv_coef(step, sqrt(*sumsq_in) * scale);
   // ring slot of this thread, stage 0 / array 0; stage stride, array stride
   const unsigned ring0 = (unsigned)__cvta_generic_to_shared(&ring[0][0][tid]);
   constexpr unsigned RS = NA * TM_THREADS * 4, RA = TM_THREADS * 4;
@@ -345,7 +359,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
     const float uu = ring[st][0][tid];
     if (!FUSED) return uu;
     const float gg = ring[st][NA - 1][tid];
-    return (float)((double)uu - coef * (double)gg);  // as tv_step_g_kernel
+    return tv_step1(uu, gg, coef);  // as tv_step_g_kernel
   };
 #pragma unroll
   for (int i = 0; i <= TM_D - 1; i++) issue();  // planes zb-1 .. zb-2+D
@@ -354,7 +368,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
   su[(zb - 1) & 1][w][lane] = uc;
   __syncthreads();
   float pz_prev = 0.f;
-  double acc = 0.0;
+  float acc = 0.f;  // fp32 partial over this thread's <= 32 planes
   float* po = gout + (ptrdiff_t)zb * (ptrdiff_t)plane + off;
   float* puo = FUSED ? uo + (ptrdiff_t)zb * (ptrdiff_t)plane + off : nullptr;
   const int wy = w < TM_WARPS - 1 ? w + 1 : w;
@@ -392,13 +406,15 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
       if (FUSED) puo += plane;
     }
     const float gs = (z >= zlo_sum && z < zhi_sum) ? g : 0.f;
-    acc += (double)gs * (double)gs;
+    acc = __fmaf_rn(gs, gs, acc);
     pz_prev = pz;
     uc = un;
   }
   cp_async_wait<0>();
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) sred[w] = acc;
+  double accd = (double)acc;
+  for (int o = 16; o > 0; o >>= 1)
+    accd += __shfl_xor_sync(0xffffffffu, accd, o);
+  if (lane == 0) sred[w] = accd;
   __syncthreads();
   if (tid == 0) {
     double sm = 0.0;
@@ -447,11 +463,8 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
   const bool own = in_xy && lane > 0 && lane < 31 && w > 0 && w < TM_WARPS - 1;
   const size_t plane = (size_t)W.nx * W.ny;
   const int off = in_xy ? y * W.nx + x : 0;
-  double coef = 0.0;
-  if (FUSED) {
-    const double norm = sqrt(*sumsq_in) * scale;
-    coef = norm < 1e-30 ? 0.0 : step / norm;  // regularization.py:148-149
-  }
+  float coef = 0.f;
+  if (FUSED) coef = tv_coef(step, sqrt(*sumsq_in) * scale);
   const unsigned ring0 = (unsigned)__cvta_generic_to_shared(&ring[0][0][tid]);
   constexpr unsigned RS = NA * TM_THREADS * 8, RA = TM_THREADS * 8;
   int zi = zb - 1;
@@ -474,8 +487,8 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
     float2 v = ring[st][0][tid];
     if (FUSED) {
       const float2 gg = ring[st][NA - 1][tid];
-      v.x = (float)((double)v.x - coef * (double)gg.x);  // as tv_step_g
-      v.y = (float)((double)v.y - coef * (double)gg.y);
+      v.x = tv_step1(v.x, gg.x, coef);  // as tv_step_g_kernel
+      v.y = tv_step1(v.y, gg.y, coef);
     }
     return v;
   };
@@ -486,7 +499,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
   su[(zb - 1) & 1][w][lane] = uc;
   __syncthreads();
   float2 pz_prev = make_float2(0.f, 0.f);
-  double acc = 0.0;
+  float acc = 0.f;  // fp32 partial over this thread's <= 64 voxels
   float2* po = reinterpret_cast<float2*>(gout + (ptrdiff_t)zb * (ptrdiff_t)plane + off);
   float2* puo = FUSED ? reinterpret_cast<float2*>(
                             uo + (ptrdiff_t)zb * (ptrdiff_t)plane + off)
@@ -530,15 +543,17 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
     }
     const bool sum = z >= zlo_sum && z < zhi_sum;
     const float sa = sum ? ga : 0.f, sb = sum ? gb : 0.f;
-    acc += (double)sa * (double)sa;
-    acc += (double)sb * (double)sb;
+    acc = __fmaf_rn(sa, sa, acc);
+    acc = __fmaf_rn(sb, sb, acc);
     pz_prev = pz;
     uc = un;
   }
   cp_async_wait<0>();
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  double accd = (double)acc;
+  for (int o = 16; o > 0; o >>= 1)
+    accd += __shfl_xor_sync(0xffffffffu, accd, o);
   __syncthreads();  // su is reused for the warp sums
-  if (lane == 0) sred[w] = acc;
+  if (lane == 0) sred[w] = accd;
   __syncthreads();
   if (tid == 0) {
     double sm = 0.0;
@@ -830,7 +845,7 @@ int reduce_into(const double* partial, size_t n, double* out,
 __global__ void sqrt_in_place_kernel(double* v) { *v = sqrt(*v); }
 
 // u_out = u - step g / ||g|| from a stored g (cs_tv_grad_store): the same
-// fp64 update as tv_gd_tiled_kernel<1>, so results are bit-identical.
+// update (tv_step1) as tv_gd_tiled_kernel<1> and the fused passes.
 __global__ void __launch_bounds__(256)
     tv_step_g_kernel(const float4* __restrict__ u,
                      const float4* __restrict__ g, float4* __restrict__ uo,
@@ -838,7 +853,7 @@ __global__ void __launch_bounds__(256)
                      double scale) {
   const double norm = sqrt(*sumsq) * scale;
   const bool skip = norm < 1e-30;  // regularization.py:148-149
-  const double coef = skip ? 0.0 : step / norm;
+  const float coef = skip ? 0.f : tv_coef(step, norm);
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
        i += (size_t)gridDim.x * blockDim.x) {
     const float4 a = __ldg(u + i);
@@ -848,10 +863,10 @@ __global__ void __launch_bounds__(256)
     }
     const float4 b = __ldg(g + i);
     float4 r;
-    r.x = (float)((double)a.x - coef * (double)b.x);
-    r.y = (float)((double)a.y - coef * (double)b.y);
-    r.z = (float)((double)a.z - coef * (double)b.z);
-    r.w = (float)((double)a.w - coef * (double)b.w);
+    r.x = tv_step1(a.x, b.x, coef);
+    r.y = tv_step1(a.y, b.y, coef);
+    r.z = tv_step1(a.z, b.z, coef);
+    r.w = tv_step1(a.w, b.w, coef);
     uo[i] = r;
   }
 }
@@ -864,10 +879,9 @@ __global__ void tv_step_g_tail_kernel(const float* __restrict__ u,
                                       double scale) {
   const double norm = sqrt(*sumsq) * scale;
   const bool skip = norm < 1e-30;
-  const double coef = skip ? 0.0 : step / norm;
+  const float coef = skip ? 0.f : tv_coef(step, norm);
   const size_t i = i0 + threadIdx.x;
-  if (i < n)
-    uo[i] = skip ? u[i] : (float)((double)u[i] - coef * (double)g[i]);
+  if (i < n) uo[i] = skip ? u[i] : tv_step1(u[i], g[i], coef);
 }
 
 static int check_win(int nx, int ny, int nzw) {

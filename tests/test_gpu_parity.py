@@ -763,9 +763,9 @@ def test_tv_stored_g_pair_bit_identical():
         K.tv_grad_store(u, g, core, s2)
         o2 = torch.empty_like(u)
         K.tv_step_g(u, g, o2, 0.05, s2, 1.3)
-        # the two kernels group the fp64 partial sums differently (the
-        # per-voxel g^2 terms are the same bits)
-        assert abs(float(s1) - float(s2)) <= 1e-12 * float(s1)
+        # the two kernels group the (fp32 per-thread) partial sums
+        # differently; the per-voxel g terms are the same bits
+        assert abs(float(s1) - float(s2)) <= 1e-6 * float(s1)
         assert torch.allclose(o1, o2, rtol=1e-6, atol=1e-7)
 
 
@@ -830,8 +830,8 @@ def test_tv_gd_vs_oracle_tiles():
 def test_tv_gd_fused_matches_tiled_kernel_subprocess():
     """The marching kernels' g equals the r01 tiled kernel's (CS_TV_TILED=1)
     bit for bit, paired (even nx) and single-voxel (CS_TV_PAIRS=0), on a
-    window with tile remainders; the fused pass agrees between the paired
-    and single-voxel kernels."""
+    window with tile remainders; the sums agree to partial-sum grouping and
+    the fused pass between the paired and single-voxel kernels to that."""
     import os
     import subprocess
     import sys
@@ -858,9 +858,12 @@ def test_tv_gd_fused_matches_tiled_kernel_subprocess():
             outs.append(torch_load(f))
     (gp, sp, up, g2p), (gs, ss, us, g2s), (gt, st, _, _) = outs
     assert (gp == gs).all() and (gp == gt).all()
-    assert (up == us).all() and (g2p == g2s).all()
+    # the fused step reads each kernel's own sum (fp32 partials grouped
+    # per kernel): equal to fp32 rounding of the step coefficient
+    assert torch.allclose(up, us, rtol=1e-6, atol=1e-7)
+    assert torch.allclose(g2p, g2s, rtol=1e-5, atol=1e-6)
     for s_ in (ss, st):
-        assert abs(float(sp) - float(s_)) <= 1e-12 * float(sp)
+        assert abs(float(sp) - float(s_)) <= 1e-6 * float(sp)
 
 
 def test_rof_vs_oracle_tiles():
