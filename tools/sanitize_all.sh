@@ -5,7 +5,7 @@ out=$1
 {
 echo "# compute-sanitizer over every kernel"
 echo
-echo 'Command: `compute-sanitizer --tool T python tools/sanitize_cases.py` on one B200 (odd sizes, slab/window launches, residual epilogue, main-axis and z-layered Ax with texture fills, Siddon, matched staged (4-CTA variant) incl. a 2 KB box budget that forces the half-depth and global fallbacks, fine-detector lane strides, FDK staged + direct path, TV-GD, ROF).'
+echo 'Command: `compute-sanitizer --tool T python tools/sanitize_cases.py` on one B200 (odd sizes, slab/window launches, residual epilogue, main-axis and z-layered Ax with texture fills, Siddon, matched staged (4-CTA 8-plane and 3-CTA 14-plane variants, x-major views in the transposed frame and in their own frame, zero-on-flush) incl. a 2 KB box budget that forces the half-depth and global fallbacks, fine-detector lane strides, FDK staged + direct path, TV-GD (r01 tiled pair and the marching gradient / fused / step passes, paired and single-voxel), ROF (marching and r01)).'
 echo
 echo "| tool | result | cases completed |"
 echo "|---|---|---|"
@@ -21,4 +21,6 @@ run "racecheck, 2 KB staged boxes" racecheck CS_STAGED_SMEM_KB=2
 run "memcheck, Ax layer pieces (CS_MAX_LAYERS=22: nx = ny = 24 in 2 pieces)" memcheck CS_MAX_LAYERS=22
 run "memcheck, Ax sub-slabs (CS_TEX_MAX_MB=0.03: 20-plane slab in 10-plane pieces; residual skipped)" memcheck CS_TEX_MAX_MB=0.03 SAN_NO_RESIDUAL=1
 run "memcheck, z-layered Ax" memcheck CS_FWD_MLAYER=0
+run "racecheck, matched x-major views in their own frame (CS_ST_TRANSPOSE=0)" racecheck CS_ST_TRANSPOSE=0
+run "memcheck, matched x-major views in their own frame (CS_ST_TRANSPOSE=0)" memcheck CS_ST_TRANSPOSE=0
 } > $out

@@ -55,6 +55,13 @@ def main():
         ss = torch.zeros(1, dtype=torch.float64, device=dev)
         K.tv_grad_sumsq(x, (0, nz), ss)
         K.tv_step(x, u2, 1e-3, ss, 1.0)
+        # marching GD kernels (paired for even nx, single-voxel for odd nx):
+        # gradient pass, fused pass, final stream step
+        g1, g2, u3 = (torch.empty_like(x) for _ in range(3))
+        s2 = torch.zeros_like(ss)
+        K.tv_grad_store(x, g1, (1, nz - 1), ss)
+        K.tv_gd_fused(x, g1, u2, g2, (1, nz - 1), 1e-3, ss, 1.0, s2)
+        K.tv_step_g(u2, g2, u3, 1e-3, s2, 1.0)
         p3 = torch.zeros((3,) + tuple(x.shape), device=dev)
         q3 = torch.empty_like(p3)
         K.rof_iter(x, p3, q3, 0.1)
@@ -68,6 +75,13 @@ def main():
     # matched Atb with strided lanes (fine pixels: lane stride 8)
     K.bwd_matched(y, g, (0, 2), (0, 8), acc)
     K.bwd_matched(y, g, (0, 2), (3, 5), acc[3:5])
+    # matched Atb on 512^2 planes: 14-plane chunks with 72 KB boxes, x-major
+    # views in the transposed frame (CS_ST_TRANSPOSE=0: in their own frame)
+    g = geometry(512, 512, 4, 96, 12, 3)
+    y = torch.from_numpy(rng.standard_normal((3, 12, 96)).astype(
+        np.float32)).to(dev)
+    acc = torch.zeros((4, 512, 512), device=dev)
+    K.bwd_matched(y, g, (0, 3), (0, 4), acc)
     torch.cuda.synchronize()
     print("sanitize cases done")
 
