@@ -240,3 +240,30 @@ def test_bench_self_launch_command():
     assert "--master-addr=127.0.0.1" in cmd and "--master-port=29501" in cmd
     i = cmd.index(os.path.join(root, "bench.py"))
     assert cmd[i + 1:] == ["--gpus", "4", "--steps", "2"]
+
+
+def test_refhook_signatures_match_reference():
+    """paper_1905_03748_b200.refhook's kernels take exactly the reference's
+    arguments (conesplit/_kernels.py:154, :213, :278, :340), so install()
+    can replace them in the reference's module.  Needs the reference
+    source (this container; absent on GPU boxes)."""
+    import importlib
+    import inspect
+    import sys
+    src = "/root/reference/pkg/src"
+    if not os.path.isdir(src):
+        pytest.skip("reference source not present")
+    sys.path.insert(0, src)
+    try:
+        try:
+            ref = importlib.import_module("conesplit._kernels")
+        except Exception as e:  # numba missing etc.
+            pytest.skip(f"reference kernels not importable: {e}")
+        from paper_1905_03748_b200 import refhook
+        for name, fn in refhook.HOOKS.items():
+            rf = getattr(ref, name)
+            rf = getattr(rf, "py_func", rf)
+            assert (list(inspect.signature(fn).parameters)
+                    == list(inspect.signature(rf).parameters)), name
+    finally:
+        sys.path.remove(src)
