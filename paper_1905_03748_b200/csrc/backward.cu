@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
           const int col = (int)fu0 - b.u0;
           const int row0 = (int)fv0 - b.v0;
           const float* base = sbox + b.off + col;
+          const f32x2 fu2 = f2(fu, fu);
           auto tap = [&](int k) {
             const float vv = fmaf((float)k, dvz, vfrac);
             const float fl = floorf(vv);
@@ -247,8 +248,11 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
             const float* q = base + (row0 + il) * b.nu;
             const float t00 = q[0], t01 = q[1];
             const float t10 = q[b.nu], t11 = q[b.nu + 1];
-            const float r0 = fmaf(fu, t01 - t00, t00);
-            const float r1 = fmaf(fu, t11 - t10, t10);
+            // both row lerps in one FADD2 + FFMA2 (bit-identical to the
+            // scalar fmaf(fu, t01 - t00, t00), fmaf(fu, t11 - t10, t10))
+            const f32x2 lo = f2(t00, t10);
+            float r0, r1;
+            f2_split(f2_fma(fu2, f2_sub(f2(t01, t11), lo), lo), r0, r1);
             acc[k] = fmaf(w2, fmaf(fv, r1 - r0, r0), acc[k]);
           };
           if (nk == FDK_ZB) {

@@ -85,29 +85,6 @@ __device__ __forceinline__ int qfloor(const March& m, int k, int axis) {
   return q_cell(q_at(m, k, axis));  // exact (common.cuh)
 }
 
-// Packed fp32 pairs (sm_100 FMUL2 / FFMA2: two lanes of fp32 per
-// instruction, each rounded exactly as the scalar op), for the matched
-// deposit's weight products and magic-add conversions.
-typedef unsigned long long f32x2;
-__device__ __forceinline__ f32x2 f2(float a, float b) {
-  f32x2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ void f2_split(f32x2 v, float& a, float& b) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ f32x2 f2_mul(f32x2 a, f32x2 b) {
-  f32x2 r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ f32x2 f2_fma(f32x2 a, f32x2 b, f32x2 c) {
-  f32x2 r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-
 // Red of a float4 quad (16-byte aligned) -- see backward.cu.
 __device__ __forceinline__ void st_red4(float* p, float a, float b, float c,
                                         float d) {
