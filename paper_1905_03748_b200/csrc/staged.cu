@@ -1075,54 +1075,52 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   // device has room for it (knob CS_ST_TRANSPOSE=0 disables).
   bool transposed = false;
   if (use_t && rows(0) > 0) {
-    {
-      double* geom_t = (double*)malloc(sizeof(double) * 12 * (size_t)n_a);
-      memcpy(geom_t, geom, sizeof(double) * 12 * (size_t)n_a);
-      for (int a = 0; a < n_a; a++)
-        for (int c = 0; c < 12; c += 3) {
-          double* g3 = geom_t + 12 * a + c;
-          const double t = g3[0];
-          g3[0] = g3[1];
-          g3[1] = t;
-        }
-      double grid6_t[6] = {grid6[1], grid6[0], grid6[2],
-                           grid6[4], grid6[3], grid6[5]};
-      const Grid GT = make_grid(grid6_t, ny, nx, nz);
-      AngleGeom* dgeom_t = nullptr;
-      float* acc_t = nullptr;
-      rc = upload_geometry(geom_t, n_a, s, &dgeom_t);
-      free(geom_t);
-      cudaError_t e2 = rc ? cudaErrorUnknown
-                          : cudaMallocAsync((void**)&acc_t, slab_bytes, s);
-      if (!rc && e2 == cudaSuccess)
-        e2 = cudaMemsetAsync(acc_t, 0, slab_bytes, s);
-      if (!rc && e2 == cudaSuccess) {
-        const int vec_t = (ny % 4 == 0);
-        k1<<<grid_of(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
-            vol_in, acc_t, dgeom_t, ids, GT, step_max, z_lo, z_hi, n_u, n_v,
-            band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_t,
-            lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad);
-        CS_COUNT_LAUNCH();
-        const dim3 tg((ny + 31) / 32, (nx + 31) / 32, z_hi - z_lo);
-        transpose_add_kernel<<<tg, dim3(32, 8), 0, s>>>(vol_acc, acc_t, nx,
-                                                        ny);
-        CS_COUNT_LAUNCH();
-        const cudaError_t e3 = cudaGetLastError();
-        cudaFreeAsync(acc_t, s);
-        release_geometry(dgeom_t, s);
-        if (e3 != cudaSuccess) {  // a launch failure is an error, not a
-          cudaFreeAsync(ids, s);  // fallback
-          release_geometry(dgeom, s);
-          CS_CHECK_CUDA(e3);
-        }
-        transposed = true;
-      } else {
-        // could not stage the transposed frame: the direct launch below
-        if (acc_t) cudaFreeAsync(acc_t, s);
-        if (dgeom_t) release_geometry(dgeom_t, s);
-        (void)cudaGetLastError();
-        rc = 0;
+    double* geom_t = (double*)malloc(sizeof(double) * 12 * (size_t)n_a);
+    memcpy(geom_t, geom, sizeof(double) * 12 * (size_t)n_a);
+    for (int a = 0; a < n_a; a++)
+      for (int c = 0; c < 12; c += 3) {
+        double* g3 = geom_t + 12 * a + c;
+        const double t = g3[0];
+        g3[0] = g3[1];
+        g3[1] = t;
       }
+    double grid6_t[6] = {grid6[1], grid6[0], grid6[2],
+                         grid6[4], grid6[3], grid6[5]};
+    const Grid GT = make_grid(grid6_t, ny, nx, nz);
+    AngleGeom* dgeom_t = nullptr;
+    float* acc_t = nullptr;
+    rc = upload_geometry(geom_t, n_a, s, &dgeom_t);
+    free(geom_t);
+    cudaError_t e2 = rc ? cudaErrorUnknown
+                        : cudaMallocAsync((void**)&acc_t, slab_bytes, s);
+    if (!rc && e2 == cudaSuccess)
+      e2 = cudaMemsetAsync(acc_t, 0, slab_bytes, s);
+    if (!rc && e2 == cudaSuccess) {
+      const int vec_t = (ny % 4 == 0);
+      k1<<<grid_of(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
+          vol_in, acc_t, dgeom_t, ids, GT, step_max, z_lo, z_hi, n_u, n_v,
+          band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_t,
+          lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad);
+      CS_COUNT_LAUNCH();
+      const dim3 tg((ny + 31) / 32, (nx + 31) / 32, z_hi - z_lo);
+      transpose_add_kernel<<<tg, dim3(32, 8), 0, s>>>(vol_acc, acc_t, nx,
+                                                      ny);
+      CS_COUNT_LAUNCH();
+      const cudaError_t e3 = cudaGetLastError();
+      cudaFreeAsync(acc_t, s);
+      release_geometry(dgeom_t, s);
+      if (e3 != cudaSuccess) {  // a launch failure is an error, not a
+        cudaFreeAsync(ids, s);  // fallback
+        release_geometry(dgeom, s);
+        CS_CHECK_CUDA(e3);
+      }
+      transposed = true;
+    } else {
+      // could not stage the transposed frame: the direct launch below
+      if (acc_t) cudaFreeAsync(acc_t, s);
+      if (dgeom_t) release_geometry(dgeom_t, s);
+      (void)cudaGetLastError();
+      rc = 0;
     }
   }
   if (!transposed && nxm > 0 && rows(0) > 0) {
