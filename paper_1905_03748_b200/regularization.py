@@ -119,13 +119,15 @@ def tv_norm(volume: Volume) -> float:
     return float(out.item())
 
 
-def _gd_iterations(u: torch.Tensor, iters: int, step: float) -> torch.Tensor:
+def _gd_iterations(u: torch.Tensor, iters: int, step: float,
+                   own: bool = False) -> torch.Tensor:
     """iters x { g = TV subgradient; u -= step g / ||g|| } on one window
-    (faces at its ends), all on device."""
+    (faces at its ends), all on device.  ``own``: u may be overwritten (the
+    caller's private copy), saving one volume."""
     nz = u.shape[0]
     if iters <= 0:
-        return u.clone()
-    a = u.clone()
+        return u if own else u.clone()
+    a = u if own else u.clone()
     b = torch.empty_like(a)
     g = torch.empty_like(a)  # g kept between the passes
     g2 = torch.empty_like(a)
@@ -150,7 +152,7 @@ def minimize_tv_gradient(volume: Volume, params: TvParams) -> Volume:
         raise ValueError("step must be positive")
     _require_nondegenerate(volume)
     u = _gd_iterations(to_device(volume.data), params.inner_iters,
-                       params.step)
+                       params.step, own=not volume.on_device)
     return _wrap(volume, u)
 
 
@@ -330,7 +332,7 @@ def _split_gd(u0: torch.Tensor, slabs: list[HaloSlab],
     if len(slabs) == 1:
         # one window == the volume: the monolithic iteration
         for _ in range(params.outer_syncs):
-            u = _gd_iterations(u, params.inner_iters, params.step)
+            u = _gd_iterations(u, params.inner_iters, params.step, own=True)
         return u
     total_voxels = u.numel()
     exact = params.norm_mode is NormMode.EXACT_GLOBAL
