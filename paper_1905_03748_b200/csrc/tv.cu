@@ -17,6 +17,9 @@
 // 28 B / voxel-iteration; the r01 per-voxel kernel for odd nx).
 #include <atomic>
 #include <cstdint>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -563,6 +566,222 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
   }
 }
 
+// TMA-fed paired variant (production when nx % 4 == 0): the same kernel
+// body as tv_march2_kernel, but each plane's 68 x 16 tile of u (and g) is
+// fetched by ONE cp.async.bulk.tensor per array, issued by thread 0 into the
+// ring stage and completed on that stage's mbarrier (out-of-range
+// coordinates -- x/y/z outside the window -- arrive as zeros, the window
+// rule); the threads only wait on the barrier and read their float2.  This
+// takes the per-thread cp.async address / predicate work (two LDGSTS and
+// ~8 integer instructions per thread and plane) off the issue-bound loop.
+constexpr int TMT_NS = 4;  // ring stages (planes in flight)
+constexpr int TMT_BOXX = 68;  // box columns: x0 - 4 .. x0 + 63
+// floats per ring slot: 68 x 16 box padded to a 128-byte multiple
+constexpr int TMT_SLOT = ((TMT_BOXX * TM_WARPS * 4 + 127) / 128) * 32;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile(
+      "mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map,
+                                            int x, int y, int z,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx"
+      "::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int FUSED>
+__global__ void __launch_bounds__(TM_THREADS, 2)
+    tv_march2_tma_kernel(const __grid_constant__ CUtensorMap map_u,
+                         const __grid_constant__ CUtensorMap map_g,
+                         float* __restrict__ uo, float* __restrict__ gout,
+                         Win W, int c_lo, int c_hi, double step,
+                         const double* __restrict__ sumsq_in, double scale,
+                         double* __restrict__ partial) {
+  constexpr int NA = FUSED ? 2 : 1;
+  constexpr unsigned TILE = TMT_BOXX * TM_WARPS * sizeof(float);  // box bytes
+  // dynamic shared memory (just over the 48 KB static limit when fused):
+  // ring | su | spy | barriers
+  extern __shared__ __align__(128) unsigned char tmt_smem[];
+  float* ring = reinterpret_cast<float*>(tmt_smem);  // [NS][NA][TMT_SLOT]
+  auto& su = *reinterpret_cast<float2(*)[2][TM_WARPS][32]>(
+      tmt_smem + sizeof(float) * TMT_NS * NA * TMT_SLOT);
+  auto& spy = *reinterpret_cast<float2(*)[2][TM_WARPS][32]>(
+      tmt_smem + sizeof(float) * TMT_NS * NA * TMT_SLOT +
+      sizeof(float2) * 2 * TM_WARPS * 32);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      tmt_smem + sizeof(float) * TMT_NS * NA * TMT_SLOT +
+      sizeof(float2) * 4 * TM_WARPS * 32);
+  double* sred = reinterpret_cast<double*>(&su[0][0][0]);  // after the loop
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tid = threadIdx.x;
+  // the box starts 16-byte aligned (a TMA requirement on the innermost
+  // coordinate): 4 columns left of the tile, 2 more than the pair lanes
+  const int xt = blockIdx.x * TM2_OX - 4, yt = blockIdx.y * TM_OY - 1;
+  const int x = xt + 2 + 2 * lane;  // pair (x, x + 1)
+  const int y = yt + w;
+  const int zb = blockIdx.z * TM_ZC;
+  const int ze = min(W.nz, zb + TM_ZC);
+  const bool in_xy = x >= 0 && x < W.nx && y >= 0 && y < W.ny;
+  const bool own = in_xy && lane > 0 && lane < 31 && w > 0 && w < TM_WARPS - 1;
+  const size_t plane = (size_t)W.nx * W.ny;
+  const int off = in_xy ? y * W.nx + x : 0;
+  float coef = 0.f;
+  if (FUSED) coef = tv_coef(step, sqrt(*sumsq_in) * scale);
+  if (tid == 0) {
+    for (int i = 0; i < TMT_NS; i++) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int zi = zb - 1;  // next plane to fetch (thread 0)
+  auto issue = [&]() {  // planes past ze are not needed
+    if (tid == 0 && zi <= ze) {
+      const int st = (zi - zb + 1) & (TMT_NS - 1);
+      mbar_expect_tx(&bars[st], NA * TILE);
+      tma_load_3d(ring + (st * NA) * TMT_SLOT, &map_u, xt, yt, zi, &bars[st]);
+      if (FUSED)
+        tma_load_3d(ring + (st * NA + 1) * TMT_SLOT, &map_g, xt, yt, zi,
+                    &bars[st]);
+    }
+    zi++;
+  };
+  auto take = [&](int zz) {
+    const int k = zz - zb + 1;  // fill index of the plane
+    const int st = k & (TMT_NS - 1);
+    mbar_wait(&bars[st], (unsigned)(k / TMT_NS) & 1u);
+    const int e = w * TMT_BOXX + 2 + 2 * lane;  // this pair in the box
+    float2 v = *reinterpret_cast<const float2*>(ring + (st * NA) * TMT_SLOT + e);
+    if (FUSED) {
+      const float2 gg =
+          *reinterpret_cast<const float2*>(ring + (st * NA + 1) * TMT_SLOT + e);
+      v.x = tv_step1(v.x, gg.x, coef);  // as tv_step_g_kernel
+      v.y = tv_step1(v.y, gg.y, coef);
+    }
+    return v;
+  };
+#pragma unroll
+  for (int i = 0; i < TMT_NS; i++) issue();  // planes zb-1 .. zb-2+NS
+  float2 uc = take(zb - 1);
+  su[(zb - 1) & 1][w][lane] = uc;
+  __syncthreads();
+  float2 pz_prev = make_float2(0.f, 0.f);
+  float acc = 0.f;  // fp32 partial over this thread's <= 64 voxels
+  float2* po = reinterpret_cast<float2*>(gout + (ptrdiff_t)zb * (ptrdiff_t)plane + off);
+  float2* puo = FUSED ? reinterpret_cast<float2*>(
+                            uo + (ptrdiff_t)zb * (ptrdiff_t)plane + off)
+                      : nullptr;
+  const size_t plane2 = plane / 2;
+  const int wy = w < TM_WARPS - 1 ? w + 1 : w;
+  const float mxa = in_xy ? 1.f : 0.f;  // x < nx - 1 holds for the even x
+  const float mxb = (in_xy && x + 1 < W.nx - 1) ? 1.f : 0.f;
+  const float my = (in_xy && y < W.ny - 1) ? 1.f : 0.f;
+  const int zlo_sum = max(zb, c_lo), zhi_sum = own ? c_hi : INT_MIN;
+  for (int z = zb - 1; z < ze; z++) {
+    // the stage of plane z was read by every thread before the previous
+    // plane's barrier: refill it (plane z + NS)
+    issue();
+    const float2 un = take(z + 1);
+    const float uxb = __shfl_down_sync(0xffffffffu, uc.x, 1);
+    const float2 uy = su[z & 1][wy][lane];
+    const float mz = (in_xy && z >= 0 && z < W.nz - 1) ? 1.f : 0.f;
+    const float gxa = (uc.y - uc.x) * mxa, gxb = (uxb - uc.y) * mxb;
+    const float gya = (uy.x - uc.x) * my, gyb = (uy.y - uc.y) * my;
+    const float gza = (un.x - uc.x) * mz, gzb = (un.y - uc.y) * mz;
+    const float ia = tv_inv_norm(gxa, gya, gza);
+    const float ib = tv_inv_norm(gxb, gyb, gzb);
+    const bool pv = in_xy && z >= 0;
+    const float pxa = __fmul_rn(gxa, ia), pxb = __fmul_rn(gxb, ib);
+    const float2 py = make_float2(__fmul_rn(gya, ia), __fmul_rn(gyb, ib));
+    const float2 pz = make_float2(pv ? __fmul_rn(gza, ia) : 0.f,
+                                  pv ? __fmul_rn(gzb, ib) : 0.f);
+    spy[z & 1][w][lane] = py;
+    su[(z + 1) & 1][w][lane] = un;
+    __syncthreads();
+    const float pxm = __shfl_up_sync(0xffffffffu, pxb, 1);
+    const float2 pym = spy[z & 1][w > 0 ? w - 1 : 0][lane];
+    const float ga = -((pz.x - pz_prev.x) + (py.x - pym.x) + (pxa - pxm));
+    const float gb = -((pz.y - pz_prev.y) + (py.y - pym.y) + (pxb - pxa));
+    if (z >= zb) {
+      if (own) {
+        *po = make_float2(ga, gb);
+        if (FUSED) *puo = uc;
+      }
+      po += plane2;
+      if (FUSED) puo += plane2;
+    }
+    const bool sum = z >= zlo_sum && z < zhi_sum;
+    const float sa = sum ? ga : 0.f, sb = sum ? gb : 0.f;
+    acc = __fmaf_rn(sa, sa, acc);
+    acc = __fmaf_rn(sb, sb, acc);
+    pz_prev = pz;
+    uc = un;
+  }
+  double accd = (double)acc;
+  for (int o = 16; o > 0; o >>= 1)
+    accd += __shfl_xor_sync(0xffffffffu, accd, o);
+  __syncthreads();  // su is reused for the warp sums
+  if (lane == 0) sred[w] = accd;
+  __syncthreads();
+  if (tid == 0) {
+    double sm = 0.0;
+    for (int i = 0; i < TM_WARPS; i++) sm += sred[i];
+    partial[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x +
+            blockIdx.x] = sm;
+  }
+}
+
+// 3D tensor map (x, y, z) of a float32 window with a 68 x 16 x 1 box
+// (cuTensorMapEncodeTiled through the runtime's driver entry point, so the
+// library needs no -lcuda); false when unavailable or the row pitch is not
+// a multiple of 16 bytes.
+static bool tv_plane_map(CUtensorMap* m, const float* base, int nx, int ny,
+                         int nz) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&fn,
+                                cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+  }
+  if (!fn || nx % 4 != 0 || ((uintptr_t)base & 15) != 0) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
+  const cuuint64_t strides[2] = {(cuuint64_t)nx * 4,
+                                 (cuuint64_t)nx * ny * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)TMT_BOXX, (cuuint32_t)TM_WARPS, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int reduce_into(const double* partial, size_t n, double* out, cudaStream_t s);
 
 // Launch the marching GD pass: the paired kernel when nx is even and every
@@ -583,7 +802,31 @@ static int launch_march(const float* u, const float* g, float* uo, float* go,
   double* part = nullptr;
   retain_pool();
   CS_CHECK_CUDA(cudaMallocAsync((void**)&part, nb * sizeof(double), s));
-  if (pairs)
+  static const char* tma_knob = getenv("CS_TV_TMA");  // A/B: 0 = cp.async
+  CUtensorMap mu, mg;
+  const bool tma = pairs && !(tma_knob && tma_knob[0] == '0') &&
+                   tv_plane_map(&mu, u, nx, ny, nzw) &&
+                   (!FUSED || tv_plane_map(&mg, g, nx, ny, nzw));
+  if (tma) {
+    constexpr int NA = FUSED ? 2 : 1;
+    const size_t smem = sizeof(float) * TMT_NS * NA * TMT_SLOT +
+                        sizeof(float2) * 4 * TM_WARPS * 32 +
+                        sizeof(uint64_t) * TMT_NS;
+    static std::atomic<unsigned long long> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_done.load() & bit)) {
+      CS_CHECK_CUDA(cudaFuncSetAttribute(
+          tv_march2_tma_kernel<FUSED>,
+          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_done.fetch_or(bit);
+    }
+    tv_march2_tma_kernel<FUSED><<<grid, TM_THREADS, smem, s>>>(
+        mu, FUSED ? mg : mu, uo, go, Win{nx, ny, nzw}, core_lo, core_hi,
+        step, sumsq_in, scale, part);
+  }
+  else if (pairs)
     tv_march2_kernel<FUSED><<<grid, TM_THREADS, 0, s>>>(
         u, g, uo, go, Win{nx, ny, nzw}, core_lo, core_hi, step, sumsq_in,
         scale, part);

@@ -780,7 +780,8 @@ def test_tv_gd_fused_bit_identical():
     # odd nx: single-voxel kernel; even nx: paired kernel (60 x 14 tiles)
     for shape, core in (((13, 11, 9), (0, 13)), ((70, 47, 65), (9, 61)),
                         ((33, 16, 32), (0, 33)), ((2, 2, 2), (0, 2)),
-                        ((70, 47, 126), (9, 61)), ((35, 29, 62), (0, 35))):
+                        ((70, 47, 126), (9, 61)), ((35, 29, 62), (0, 35)),
+                        ((37, 29, 132), (3, 30)), ((41, 19, 64), (0, 41))):
         u = torch.rand(shape, device="cuda", generator=gen)
         g = torch.empty_like(u)
         s0 = torch.zeros(1, dtype=torch.float64, device="cuda")
@@ -840,30 +841,35 @@ def test_tv_gd_fused_matches_tiled_kernel_subprocess():
         "import torch,sys;sys.path.insert(0,'.');"
         "from paper_1905_03748_b200 import kernels as K;"
         "gen=torch.Generator(device='cuda').manual_seed(3);"
-        "u=torch.rand((45,38,70),device='cuda',generator=gen);"
+        "u=torch.rand((45,38,int(sys.argv[2])),device='cuda',generator=gen);"
         "g=torch.empty_like(u);s=torch.zeros(1,dtype=torch.float64,"
         "device='cuda');K.tv_grad_store(u,g,(4,40),s);"
         "u2=torch.empty_like(u);g2=torch.empty_like(u);s2=torch.zeros_like(s);"
         "K.tv_gd_fused(u,g,u2,g2,(4,40),0.05,s,1.0,s2);"
         "torch.save((g.cpu(),s.cpu(),u2.cpu(),g2.cpu()),sys.argv[1])")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    with tempfile.TemporaryDirectory() as td:
-        outs = []
-        for tag, env_add in (("pairs", {}), ("single", {"CS_TV_PAIRS": "0"}),
-                             ("tiled", {"CS_TV_TILED": "1"})):
-            f = os.path.join(td, f"{tag}.pt")
-            env = dict(os.environ, **env_add)
-            subprocess.run([sys.executable, "-c", code, f], cwd=root,
-                           env=env, check=True)
-            outs.append(torch_load(f))
-    (gp, sp, up, g2p), (gs, ss, us, g2s), (gt, st, _, _) = outs
-    assert (gp == gs).all() and (gp == gt).all()
-    # the fused step reads each kernel's own sum (fp32 partials grouped
-    # per kernel): equal to fp32 rounding of the step coefficient
-    assert torch.allclose(up, us, rtol=1e-6, atol=1e-7)
-    assert torch.allclose(g2p, g2s, rtol=1e-5, atol=1e-6)
-    for s_ in (ss, st):
-        assert abs(float(sp) - float(s_)) <= 1e-6 * float(sp)
+    # nx = 70: paired kernel fed by cp.async; nx = 132: paired kernel fed by
+    # TMA (nx % 4 == 0), against the cp.async feed (CS_TV_TMA=0)
+    for nx, variants in ((70, (("pairs", {}), ("single", {"CS_TV_PAIRS": "0"}),
+                               ("tiled", {"CS_TV_TILED": "1"}))),
+                         (132, (("tma", {}), ("cpasync", {"CS_TV_TMA": "0"}),
+                                ("tiled", {"CS_TV_TILED": "1"})))):
+        with tempfile.TemporaryDirectory() as td:
+            outs = []
+            for tag, env_add in variants:
+                f = os.path.join(td, f"{tag}.pt")
+                env = dict(os.environ, **env_add)
+                subprocess.run([sys.executable, "-c", code, f, str(nx)],
+                               cwd=root, env=env, check=True)
+                outs.append(torch_load(f))
+        (gp, sp, up, g2p), (gs, ss, us, g2s), (gt, st, _, _) = outs
+        assert (gp == gs).all() and (gp == gt).all(), nx
+        # the fused step reads each kernel's own sum (fp32 partials grouped
+        # per kernel): equal to fp32 rounding of the step coefficient
+        assert torch.allclose(up, us, rtol=1e-6, atol=1e-7), nx
+        assert torch.allclose(g2p, g2s, rtol=1e-5, atol=1e-6), nx
+        for s_ in (ss, st):
+            assert abs(float(sp) - float(s_)) <= 1e-6 * float(sp), nx
 
 
 def test_rof_vs_oracle_tiles():
