@@ -938,15 +938,31 @@ __global__ void __launch_bounds__(256)
 constexpr int RM_NS = 4;
 constexpr int RM_D = RM_NS - 1;
 
+// TMA: the four arrays of each plane arrive as 68 x 16 tensor boxes
+// (one cp.async.bulk.tensor per array, issued by thread 0 into an mbarrier
+// ring stage), as in tv_march2_tma_kernel; else per-thread cp.async.
+struct RofMaps {
+  CUtensorMap f, pz, py, px;
+};
+
+template <bool TMA>
 __global__ void __launch_bounds__(TM_THREADS, 2)
     rof_march2_kernel(const float* __restrict__ f, const float* __restrict__ pin,
                       float* __restrict__ pout, Win W, float lam,
-                      float tau_over_lam) {
-  extern __shared__ float2 rm_ring[];  // [RM_NS][4][TM_THREADS]: f pz py px
+                      float tau_over_lam,
+                      const __grid_constant__ RofMaps maps) {
+  // dynamic: cp.async ring float2[RM_NS][4][TM_THREADS] (f pz py px), or
+  // the TMA ring float[RM_NS][4][TMT_SLOT] + RM_NS mbarriers
+  extern __shared__ __align__(128) unsigned char rm_smem[];
+  float2* rm_ring = reinterpret_cast<float2*>(rm_smem);
+  float* tm_ring = reinterpret_cast<float*>(rm_smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      rm_smem + sizeof(float) * RM_NS * 4 * TMT_SLOT);
   __shared__ float2 su[2][TM_WARPS][32];
   __shared__ float2 spy[2][TM_WARPS][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int tid = threadIdx.x;
+  const int xt = blockIdx.x * TM2_OX - 4, yt = blockIdx.y * TM_OY - 1;
   const int x = blockIdx.x * TM2_OX - 2 + 2 * lane;  // pair (x, x + 1)
   const int y = blockIdx.y * TM_OY - 1 + w;
   const int zb = blockIdx.z * TM_ZC;
@@ -963,24 +979,55 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
   int zi = zb - 1;
   const float* pf = f + (ptrdiff_t)zi * (ptrdiff_t)plane + off;
   const float* pp = pin + (ptrdiff_t)zi * (ptrdiff_t)plane + off;
+  if (TMA) {
+    if (tid == 0) {
+      for (int i = 0; i < RM_NS; i++) mbar_init(&bars[i], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   auto issue = [&]() {
-    const bool ok = in_xy && (unsigned)zi < (unsigned)W.nz;
-    const unsigned st = ring0 + ((zi - zb + 1) & (RM_NS - 1)) * RS;
-    cp_async8(st, ok ? pf : f, ok);
-    cp_async8(st + RA, ok ? pp : f, ok);
-    cp_async8(st + 2 * RA, ok ? pp + vol : f, ok);
-    cp_async8(st + 3 * RA, ok ? pp + 2 * vol : f, ok);
-    cp_async_commit();
+    const int st = (zi - zb + 1) & (RM_NS - 1);
+    if (TMA) {
+      if (tid == 0) {
+        constexpr unsigned BOX = TMT_BOXX * TM_WARPS * sizeof(float);
+        float* dst = tm_ring + st * 4 * TMT_SLOT;
+        mbar_expect_tx(&bars[st], 4 * BOX);
+        tma_load_3d(dst, &maps.f, xt, yt, zi, &bars[st]);
+        tma_load_3d(dst + TMT_SLOT, &maps.pz, xt, yt, zi, &bars[st]);
+        tma_load_3d(dst + 2 * TMT_SLOT, &maps.py, xt, yt, zi, &bars[st]);
+        tma_load_3d(dst + 3 * TMT_SLOT, &maps.px, xt, yt, zi, &bars[st]);
+      }
+    } else {
+      const bool ok = in_xy && (unsigned)zi < (unsigned)W.nz;
+      const unsigned sa = ring0 + st * RS;
+      cp_async8(sa, ok ? pf : f, ok);
+      cp_async8(sa + RA, ok ? pp : f, ok);
+      cp_async8(sa + 2 * RA, ok ? pp + vol : f, ok);
+      cp_async8(sa + 3 * RA, ok ? pp + 2 * vol : f, ok);
+      cp_async_commit();
+      pf += plane;
+      pp += plane;
+    }
     zi++;
-    pf += plane;
-    pp += plane;
   };
   auto take = [&](int zz, float2& fv, float2& pz, float2& py, float2& px) {
-    const float2* r = rm_ring + ((zz - zb + 1) & (RM_NS - 1)) * 4 * TM_THREADS + tid;
-    fv = r[0];
-    pz = r[TM_THREADS];
-    py = r[2 * TM_THREADS];
-    px = r[3 * TM_THREADS];
+    const int k = zz - zb + 1;
+    const int st = k & (RM_NS - 1);
+    if (TMA) {
+      mbar_wait(&bars[st], (unsigned)(k / RM_NS) & 1u);
+      const float* r = tm_ring + st * 4 * TMT_SLOT + w * TMT_BOXX + 2 + 2 * lane;
+      fv = *reinterpret_cast<const float2*>(r);
+      pz = *reinterpret_cast<const float2*>(r + TMT_SLOT);
+      py = *reinterpret_cast<const float2*>(r + 2 * TMT_SLOT);
+      px = *reinterpret_cast<const float2*>(r + 3 * TMT_SLOT);
+    } else {
+      const float2* r = rm_ring + st * 4 * TM_THREADS + tid;
+      fv = r[0];
+      pz = r[TM_THREADS];
+      py = r[2 * TM_THREADS];
+      px = r[3 * TM_THREADS];
+    }
   };
 #pragma unroll
   for (int i = 0; i <= RM_D - 1; i++) issue();  // planes zb-1 .. zb-2+D
@@ -993,10 +1040,10 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
   for (int z = zb - 2; z < ze; z++) {
     if (z + 1 + RM_D <= ze) {  // planes up to ze; empty groups keep the count
       issue();
-    } else {
+    } else if (!TMA) {
       cp_async_commit();
     }
-    cp_async_wait<RM_D>();  // plane z + 1 landed (own slots only)
+    if (!TMA) cp_async_wait<RM_D>();  // plane z + 1 landed (own slots only)
     float2 f1, pz1, py1, px1;
     take(z + 1, f1, pz1, py1, px1);
     spy[(z + 1) & 1][w][lane] = py1;
@@ -1281,21 +1328,44 @@ int cs_rof_iter(const float* f, const float* p_in, float* p_out, int nx,
                      (uintptr_t)f % 8 == 0 && (uintptr_t)p_in % 8 == 0 &&
                      (uintptr_t)p_out % 8 == 0;
   if (march) {
-    const size_t smem = (size_t)RM_NS * 4 * TM_THREADS * sizeof(float2);
+    // TMA feed when every array qualifies (nx % 4 == 0, 16-byte bases)
+    static const char* tma_knob = getenv("CS_TV_TMA");  // A/B: 0 = cp.async
+    const size_t vol = (size_t)nx * ny * nzw;
+    RofMaps maps;
+    const bool tma = !(tma_knob && tma_knob[0] == '0') &&
+                     tv_plane_map(&maps.f, f, nx, ny, nzw) &&
+                     tv_plane_map(&maps.pz, p_in, nx, ny, nzw) &&
+                     tv_plane_map(&maps.py, p_in + vol, nx, ny, nzw) &&
+                     tv_plane_map(&maps.px, p_in + 2 * vol, nx, ny, nzw);
+    const size_t smem =
+        tma ? sizeof(float) * RM_NS * 4 * TMT_SLOT + sizeof(uint64_t) * RM_NS
+            : (size_t)RM_NS * 4 * TM_THREADS * sizeof(float2);
     static std::atomic<unsigned long long> attr_done{0};
     int dev = 0;
     cudaGetDevice(&dev);
     const unsigned long long bit = 1ull << (dev & 63);
     if (!(attr_done.load() & bit)) {
+      const int big = (int)(sizeof(float) * RM_NS * 4 * TMT_SLOT +
+                            sizeof(uint64_t) * RM_NS);
       CS_CHECK_CUDA(cudaFuncSetAttribute(
-          rof_march2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-          (int)smem));
+          rof_march2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+          big));
+      CS_CHECK_CUDA(cudaFuncSetAttribute(
+          rof_march2_kernel<false>,
+          cudaFuncAttributeMaxDynamicSharedMemorySize,
+          (int)((size_t)RM_NS * 4 * TM_THREADS * sizeof(float2))));
       attr_done.fetch_or(bit);
     }
     const dim3 grid((nx + TM2_OX - 1) / TM2_OX, (ny + TM_OY - 1) / TM_OY,
                     (nzw + TM_ZC - 1) / TM_ZC);
-    rof_march2_kernel<<<grid, TM_THREADS, smem, s>>>(
-        f, p_in, p_out, Win{nx, ny, nzw}, (float)lam, (float)(ROF_TAU / lam));
+    if (tma)
+      rof_march2_kernel<true><<<grid, TM_THREADS, smem, s>>>(
+          f, p_in, p_out, Win{nx, ny, nzw}, (float)lam,
+          (float)(ROF_TAU / lam), maps);
+    else
+      rof_march2_kernel<false><<<grid, TM_THREADS, smem, s>>>(
+          f, p_in, p_out, Win{nx, ny, nzw}, (float)lam,
+          (float)(ROF_TAU / lam), maps);
   } else {
     const dim3 grid((nx + 31) / 32, (ny + 7) / 8, nzw);
     rof_iter_kernel<<<grid, dim3(32, 8), 0, s>>>(

@@ -876,7 +876,7 @@ def test_rof_vs_oracle_tiles():
     """minimize_rof against the oracle on volumes spanning several 60 x 14 x
     32 tiles (marching kernel, even nx) and with odd nx (r01 kernel)."""
     rng = np.random.default_rng(12)
-    for nx in (126, 65):
+    for nx in (126, 65, 132):  # cp.async feed, r01 kernel, TMA feed
         f = rng.random((70, 47, nx), dtype=np.float32)
         vol = cs.Volume(cs.VoxelGrid(nx, 47, 70), f)
         got = cs.minimize_rof(vol, cs.TvParams(cs.TvMinimizer.ROF,
@@ -899,21 +899,27 @@ def test_rof_march_bit_identical_subprocess():
         "import torch,sys;sys.path.insert(0,'.');"
         "from paper_1905_03748_b200 import kernels as K;"
         "gen=torch.Generator(device='cuda').manual_seed(5);"
-        "f=torch.rand((45,38,70),device='cuda',generator=gen);"
-        "p=torch.rand((3,45,38,70),device='cuda',generator=gen)-0.5;"
+        "nx=int(sys.argv[2]);"
+        "f=torch.rand((45,38,nx),device='cuda',generator=gen);"
+        "p=torch.rand((3,45,38,nx),device='cuda',generator=gen)-0.5;"
         "q=torch.empty_like(p);K.rof_iter(f,p,q,0.2);"
         "q2=torch.empty_like(p);K.rof_iter(f,q,q2,0.2);"
         "torch.save((q.cpu(),q2.cpu()),sys.argv[1])")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    with tempfile.TemporaryDirectory() as td:
-        outs = []
-        for tag, env_add in (("march", {}), ("r01", {"CS_ROF_MARCH": "0"})):
-            fn = os.path.join(td, f"{tag}.pt")
-            subprocess.run([sys.executable, "-c", code, fn], cwd=root,
-                           env=dict(os.environ, **env_add), check=True)
-            outs.append(torch_load(fn))
-    (a1, a2), (b1, b2) = outs
-    assert (a1 == b1).all() and (a2 == b2).all()
+    # nx = 70: cp.async feed; nx = 132: TMA feed (and its cp.async twin)
+    for nx in (70, 132):
+        with tempfile.TemporaryDirectory() as td:
+            outs = []
+            for tag, env_add in (("march", {}), ("cpasync", {"CS_TV_TMA": "0"}),
+                                 ("r01", {"CS_ROF_MARCH": "0"})):
+                fn = os.path.join(td, f"{tag}.pt")
+                subprocess.run([sys.executable, "-c", code, fn, str(nx)],
+                               cwd=root, env=dict(os.environ, **env_add),
+                               check=True)
+                outs.append(torch_load(fn))
+        (a1, a2), (b1, b2), (c1, c2) = outs
+        assert (a1 == c1).all() and (a2 == c2).all(), nx
+        assert (b1 == c1).all() and (b2 == c2).all(), nx
 
 
 def test_matched_transposed_frame_subprocess():
