@@ -46,6 +46,8 @@ KEYS = {"fwd_mlayer": "fwd_mlayer_kernel", "fill_xlayers": "fwd_mlayer_kernel",
         "fwd_siddon": "fwd_siddon_kernel",
         "tv_march2_kernel<1": "tv_gd_fused_kernel",
         "tv_march2_kernel<0": "tv_grad_kernel",
+        "tv_march2_tma_kernel<1": "tv_gd_fused_kernel",
+        "tv_march2_tma_kernel<0": "tv_grad_kernel",
         "rof_march2": "rof_iter_kernel"}
 
 
