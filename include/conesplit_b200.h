@@ -144,7 +144,8 @@ int cs_tv_step(const float* u, float* u_out, int nx, int ny, int nzw,
  * n voxels -- the same g and the same step arithmetic as cs_tv_grad_sumsq
  * + cs_tv_step (the sums agree to fp32 partial-sum grouping), with the
  * second pass a stream instead of a second stencil.  The step is
- * u - c g with c = step / norm rounded once to fp32 (one FFMA). */
+ * u - c g with c = step / norm rounded once to fp32 (one FFMA);
+ * cs_tv_step_g may write in place (u_out == u), not over g. */
 int cs_tv_grad_store(const float* u, float* g, int nx, int ny, int nzw,
                      int core_lo, int core_hi, double* out_sum,
                      cs_stream_t stream);

@@ -1289,8 +1289,8 @@ int cs_tv_step_g(const float* u, const float* g, float* u_out, int64_t n,
                  double step, const double* norm_sumsq_dev, double scale,
                  cs_stream_t stream) {
   CS_REQUIRE(n >= 0, CS_ERR_ARG, "negative length");
-  CS_REQUIRE(u != u_out && g != u_out, CS_ERR_ARG,
-             "cs_tv_step_g: u_out aliases an input");
+  // elementwise: u_out may be u (in place); not g
+  CS_REQUIRE(g != u_out, CS_ERR_ARG, "cs_tv_step_g: u_out aliases g");
   cudaStream_t s = (cudaStream_t)stream;
   const bool vec = ((uintptr_t)u % 16 == 0) && ((uintptr_t)g % 16 == 0) &&
                    ((uintptr_t)u_out % 16 == 0);

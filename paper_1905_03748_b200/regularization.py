@@ -267,20 +267,40 @@ def _split_gd_streamed(u: np.ndarray, slabs: list[HaloSlab],
     ss = torch.zeros(1, dtype=torch.float64, device=dev)
     for _ in range(params.outer_syncs):
         local = [u[s.window[0]:s.window[1]].copy() for s in slabs]
-        if exact:
-            for _ in range(params.inner_iters):
-                sums = torch.zeros(len(slabs), dtype=torch.float64,
-                                   device=dev)
-                for i, (s, w) in enumerate(zip(slabs, local)):
-                    c = s.core_in_window
-                    K.tv_grad_sumsq(_h2d(w), (c.start, c.stop),
-                                    sums[i:i + 1])
+        if exact and params.inner_iters > 0:
+            # One pass over the windows per iteration (plus one for the
+            # first sums): each window, held in page-locked memory, is
+            # uploaded once, its gradient recomputed and the step taken in
+            # place with the global norm (cs_tv_grad_store, cs_tv_step_g),
+            # the next iteration's sums formed from the stepped window
+            # (cs_tv_grad_store again, into the same g), and the window
+            # drained back: one upload instead of two per window and
+            # iteration, and the two window-sized device buffers the
+            # planner assumed (regularization.py:197-210).
+            n = len(slabs)
+            pin = [torch.from_numpy(w).pin_memory() for w in local]
+            cores = [(s.core_in_window.start, s.core_in_window.stop)
+                     for s in slabs]
+            sums = torch.zeros(n, dtype=torch.float64, device=dev)
+            for i in range(n):
+                K.tv_grad_sumsq(pin[i].to(dev, non_blocking=True), cores[i],
+                                sums[i:i + 1])
+            scratch = torch.zeros(1, dtype=torch.float64, device=dev)
+            for it in range(params.inner_iters):
                 tot = sums.sum().reshape(1)
-                for i, w in enumerate(local):
-                    wd = _h2d(w)
-                    out = torch.empty_like(wd)
-                    K.tv_step(wd, out, params.step, tot, 1.0)
-                    local[i] = out.cpu().numpy()
+                last = it == params.inner_iters - 1
+                nxt = torch.zeros(n, dtype=torch.float64, device=dev)
+                for i in range(n):
+                    wd = pin[i].to(dev, non_blocking=True)
+                    g = torch.empty_like(wd)
+                    K.tv_grad_store(wd, g, cores[i], scratch)
+                    K.tv_step_g(wd, g, wd, params.step, tot, 1.0)
+                    if not last:
+                        K.tv_grad_store(wd, g, cores[i], nxt[i:i + 1])
+                    pin[i].copy_(wd, non_blocking=True)
+                    torch.cuda.current_stream(dev).synchronize()
+                sums = nxt
+            local = [t.numpy() for t in pin]
         else:
             for i, w in enumerate(local):
                 wd = _h2d(w)
