@@ -500,7 +500,12 @@ def run_config3(args, rank, world, local, backend):
         "config": {"workload": c3_workload(args, world),
                    "l2": "inputs > L2 (volume slabs >= 4 GiB)",
                    "parallelism": f"slab x{world} / angle shard x{world}",
-                   "backend": backend},
+                   "backend": backend,
+                   # peer: partial sums stored by the Ax kernels into the
+                   # owners' memory, matched Atb reading the owners' views
+                   # in place (peer.py); collective: NCCL reduce-scatter /
+                   # all-gather per round (CS_EXCHANGE=nccl)
+                   "exchange": ops.exchange_mode},
     })
     del np, K
     return res

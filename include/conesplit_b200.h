@@ -206,6 +206,24 @@ int cs_weighted_residual(float* r, const float* b, const float* w, int64_t n,
 /* x = value */
 int cs_fill(float* x, float value, int64_t n, cs_stream_t stream);
 
+/* ------------------------------------------- sharded peer exchange ---- */
+
+/* out[i] = sum_{k < n_src} src[k * stride + i], summed in k order; with b:
+ * out = b - sum, with b and w: out = w * (b - sum).  The owner-side half of
+ * the slab-sharded forward's peer exchange (sharded.py / peer.py): the
+ * other ranks' kernels stored their partial projections of the owner's
+ * views into the owner's inbox slices (replaces the reduce-scatter of the
+ * partials, the reference's slab-partial sum execution.py:224-235, fused
+ * with OS-SART's residual algorithms.py:296-297). */
+int cs_sum_slices(const float* src, int n_src, int64_t stride, int64_t n,
+                  const float* b, const float* w, float* out,
+                  cs_stream_t stream);
+/* Lets kernels on the current device load / store device memory of
+ * `peer_device` (cudaDeviceEnablePeerAccess; already enabled or
+ * peer == current is fine).  CS_ERR_UNSUPPORTED when the pair has no P2P
+ * path. */
+int cs_peer_enable(int peer_device);
+
 #ifdef __cplusplus
 }
 #endif

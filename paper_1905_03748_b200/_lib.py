@@ -66,6 +66,8 @@ SYMBOLS: dict[str, list] = {
     "cs_sart_update": [P, P, P, D, L, P],
     "cs_weighted_residual": [P, P, P, L, P],
     "cs_fill": [P, ctypes.c_float, L, P],
+    "cs_sum_slices": [P, I, L, L, P, P, P, P],
+    "cs_peer_enable": [I],
 }
 
 _lib = None

@@ -294,4 +294,24 @@ int cs_release_cache(void) {
   return CS_OK;
 }
 
+int cs_peer_enable(int peer_device) {
+  int dev = 0, n = 0;
+  CS_CHECK_CUDA(cudaGetDevice(&dev));
+  CS_CHECK_CUDA(cudaGetDeviceCount(&n));
+  CS_REQUIRE(peer_device >= 0 && peer_device < n, CS_ERR_ARG,
+             "peer device %d out of range (%d devices)", peer_device, n);
+  if (peer_device == dev) return CS_OK;
+  int ok = 0;
+  CS_CHECK_CUDA(cudaDeviceCanAccessPeer(&ok, dev, peer_device));
+  CS_REQUIRE(ok, CS_ERR_UNSUPPORTED, "no P2P path from device %d to %d", dev,
+             peer_device);
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return CS_OK;
+  }
+  CS_CHECK_CUDA(e);
+  return CS_OK;
+}
+
 }  // extern "C"

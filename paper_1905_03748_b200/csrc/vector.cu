@@ -103,6 +103,66 @@ __global__ void weighted_residual_kernel(float* __restrict__ r,
   }
 }
 
+// Sum of n_src equally strided slices in slice order (deterministic), and
+// optionally the OS-SART residual of the sum: out = w o (b - sum).  The
+// owner-side half of the sharded forward's peer exchange (sharded.py): the
+// slices are the partial projections the other ranks stored into this
+// rank's inbox.  float4 lanes when every base and the stride are 16-byte
+// aligned (sheets of n_u n_v floats with n_u n_v % 4 == 0), else scalar.
+template <typename T>
+__device__ __forceinline__ T ld_slice(const float* p, int64_t i) {
+  return reinterpret_cast<const T*>(p)[i];
+}
+
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
+__device__ __forceinline__ float4 f4_res(float4 b, float4 s) {
+  return make_float4(b.x - s.x, b.y - s.y, b.z - s.z, b.w - s.w);
+}
+
+__device__ __forceinline__ float4 f4_mul(float4 a, float4 b) {
+  return make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w);
+}
+
+__global__ void __launch_bounds__(256)
+    sum_slices4_kernel(const float* __restrict__ src, int n_src,
+                       int64_t stride4, int64_t n4,
+                       const float* __restrict__ b,
+                       const float* __restrict__ w, float* __restrict__ out) {
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += step) {
+    float4 s = ld_slice<float4>(src, i);
+    for (int k = 1; k < n_src; k++)
+      s = f4_add(s, ld_slice<float4>(src, k * stride4 + i));
+    if (b) {
+      s = f4_res(ld_slice<float4>(b, i), s);
+      if (w) s = f4_mul(ld_slice<float4>(w, i), s);
+    }
+    reinterpret_cast<float4*>(out)[i] = s;
+  }
+}
+
+__global__ void sum_slices_kernel(const float* __restrict__ src, int n_src,
+                                  int64_t stride, int64_t n,
+                                  const float* __restrict__ b,
+                                  const float* __restrict__ w,
+                                  float* __restrict__ out) {
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += step) {
+    float s = src[i];
+    for (int k = 1; k < n_src; k++) s += src[k * stride + i];
+    if (b) {
+      s = b[i] - s;
+      if (w) s = w[i] * s;
+    }
+    out[i] = s;
+  }
+}
+
 __global__ void fill_kernel(float* __restrict__ x, float value, int64_t n) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -182,6 +242,29 @@ int cs_weighted_residual(float* r, const float* b, const float* w, int64_t n,
   if (n <= 0) return CS_OK;
   weighted_residual_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
       r, b, w, n);
+  CS_COUNT_LAUNCH();
+  CS_CHECK_CUDA(cudaGetLastError());
+  return CS_OK;
+}
+
+int cs_sum_slices(const float* src, int n_src, int64_t stride, int64_t n,
+                  const float* b, const float* w, float* out,
+                  cs_stream_t stream) {
+  if (n <= 0) return CS_OK;
+  CS_REQUIRE(n_src >= 1 && src && out && (b || !w), CS_ERR_ARG,
+             "sum_slices: need n_src >= 1, src, out (and b with w)");
+  auto al = [](const void* p) {
+    return ((uintptr_t)p & 15) == 0;
+  };
+  const cudaStream_t s = (cudaStream_t)stream;
+  if (n % 4 == 0 && stride % 4 == 0 && al(src) && al(out) &&
+      (!b || al(b)) && (!w || al(w))) {
+    sum_slices4_kernel<<<grid_for(n / 4), 256, 0, s>>>(src, n_src, stride / 4,
+                                                       n / 4, b, w, out);
+  } else {
+    sum_slices_kernel<<<grid_for(n), 256, 0, s>>>(src, n_src, stride, n, b, w,
+                                                  out);
+  }
   CS_COUNT_LAUNCH();
   CS_CHECK_CUDA(cudaGetLastError());
   return CS_OK;

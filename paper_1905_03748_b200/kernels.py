@@ -315,6 +315,32 @@ def weighted_residual(r, b, w, stream=None):
     return r
 
 
+def sum_slices(src: torch.Tensor, out: torch.Tensor,
+               b: torch.Tensor | None = None, w: torch.Tensor | None = None,
+               stream=None) -> torch.Tensor:
+    """out = sum_k src[k] in k order (src: (n_src,) + out.shape, each
+    slice contiguous); with b: out = b - sum, with b and w: w * (b - sum)."""
+    n = out.numel()
+    _f32(out, "out")
+    assert src.shape[1:] == out.shape, (src.shape, out.shape)
+    assert src.shape[0] >= 1 and src.dtype == torch.float32
+    assert src.shape[0] == 1 or src.stride(0) >= n
+    for t, name in ((b, "b"), (w, "w")):
+        if t is not None:
+            _f32(t, name)
+            assert t.shape == out.shape
+    check(lib().cs_sum_slices(dptr(src[0]), src.shape[0], src.stride(0), n,
+                              None if b is None else dptr(b),
+                              None if w is None else dptr(w), dptr(out),
+                              stream_ptr(stream)))
+    return out
+
+
+def peer_enable(device_index: int) -> None:
+    """Let kernels on the current device reach memory of ``device_index``."""
+    check(lib().cs_peer_enable(int(device_index)))
+
+
 def fill(x, value: float, stream=None):
     check(lib().cs_fill(dptr(x), float(value), x.numel(), stream_ptr(stream)))
     return x

@@ -183,6 +183,35 @@ class ShardedOperators:
         self._fwd = (self.kernels.fwd_interp
                      if self.method is ProjectionMethod.INTERPOLATED
                      else self.kernels.fwd_siddon)
+        self._peer = None
+        self._peer_tried = False
+
+    def exchange(self, like: torch.Tensor | None = None):
+        """The peer exchange (peer.py) when it is in use, else None (NCCL's
+        collectives).  Set up on the first multi-rank operator call -- a
+        collective, so every rank reaches it in the same call -- when the
+        tensors are CUDA tensors and the kernels are the sm_100a ones."""
+        if self._peer_tried or self.world == 1:
+            return self._peer
+        if like is None or not like.is_cuda or \
+                self.kernels is not _CudaKernels:
+            return None
+        from .peer import PeerExchange, peer_mode_requested
+        self._peer_tried = True
+        if not peer_mode_requested():
+            return None
+        group = None if not _nccl() else dist.new_group(backend="gloo")
+        det = self.geometry.detector
+        self._peer = PeerExchange.create(
+            self.rank, self.world, like.device, self.round_views,
+            (det.n_v, det.n_u), group)
+        return self._peer
+
+    @property
+    def exchange_mode(self) -> str:
+        if self.world == 1:
+            return "none"
+        return "peer" if self._peer is not None else "collective"
 
     def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
         """Sum a (scalar) tensor over the ranks; identity on one rank."""
@@ -216,6 +245,8 @@ class ShardedOperators:
             if a1 > a0:
                 self._fwd(x_slab, self.geometry, (a0, a1), (z0, z1), out)
             return out
+        if self.exchange(x_slab) is not None:
+            return self._forward_peer(x_slab, out, angle_range)
         shards, c, rounds = self._rounds(angle_range)
         m0, _ = shards[self.rank]
         bufs = [self._sheet(self.world * c, out) for _ in range(min(2, rounds))]
@@ -251,6 +282,43 @@ class ShardedOperators:
                 land(p)
         return out
 
+    def _forward_peer(self, x_slab, out, angle_range, b=None, w=None):
+        """forward over peer memory (peer.py): per round, this rank's Ax
+        kernels store the partials of shard s straight into rank s's inbox
+        slot (P2P stores); after the round's barrier the side stream sums
+        this rank's inbox in rank order into ``out`` (with b / w: the
+        residual w o (b - sum)) while the compute stream moves on."""
+        X = self._peer
+        z0, z1 = self.slab
+        shards, c, rounds = self._rounds(angle_range)
+        m0, m1 = shards[self.rank]
+        cur = torch.cuda.current_stream()
+        X.side.wait_stream(cur)          # out / b / w are ready on cur
+        for j in range(rounds):
+            slot = X.next_slot("fwd")
+            for s, (s0, s1) in enumerate(shards):
+                c0, c1 = s0 + j * c, min(s0 + (j + 1) * c, s1)
+                if c1 <= c0:
+                    continue
+                cur.wait_event(X.peer_ev[s]["consumed"][slot])
+                part = X.inboxes[s][slot, self.rank, :c1 - c0]
+                if z1 > z0:
+                    self._fwd(x_slab, self.geometry, (c0, c1), (z0, z1), part)
+                else:
+                    K.fill(part, 0.0)
+            X.record(cur, "written", slot)
+            X.barrier()
+            lo, hi = m0 + j * c, min(m0 + (j + 1) * c, m1)
+            if hi > lo:
+                X.wait_all(X.side, "written", slot)
+                rows = slice(lo - m0, hi - m0)
+                K.sum_slices(X.inbox[slot, :, :hi - lo], out[rows],
+                             None if b is None else b[rows],
+                             None if w is None else w[rows], stream=X.side)
+            X.record(X.side, "consumed", slot)
+        cur.wait_stream(X.side)
+        return out
+
     def forward_residual(self, x_slab: torch.Tensor, b: torch.Tensor,
                          w: torch.Tensor | None, out: torch.Tensor,
                          angle_range) -> torch.Tensor:
@@ -269,6 +337,8 @@ class ShardedOperators:
             except ConesplitCudaError as e:
                 if e.code != -3:  # CS_ERR_UNSUPPORTED: nz > layer limit
                     raise
+        if self.world > 1 and self.exchange(x_slab) is not None:
+            return self._forward_peer(x_slab, out, angle_range, b, w)
         self.forward(x_slab, out, angle_range)
         return self._vec_residual(out, b, w)
 
@@ -288,6 +358,8 @@ class ShardedOperators:
                 self.kernels.bwd_matched(y, self.geometry, (a0, a1), (z0, z1),
                                          out_slab)
             return out_slab
+        if self.exchange(y) is not None:
+            return self._backward_peer(y, out_slab, angle_range)
         shards, c, rounds = self._rounds(angle_range)
         m0, m1 = shards[self.rank]
         nbuf = min(2, rounds)
@@ -314,6 +386,37 @@ class ShardedOperators:
                             g[s * c:s * c + (c1 - c0)], self.geometry,
                             (c0, c1), (z0, z1), out_slab)
             work = nxt
+        return out_slab
+
+    def _backward_peer(self, y, out_slab, angle_range):
+        """backward over peer memory: per round, the side stream stages this
+        rank's views in its outbox slot (once every reader of the slot's
+        previous round is done); after the barrier the matched kernels read
+        every owner's outbox in place (P2P loads)."""
+        X = self._peer
+        z0, z1 = self.slab
+        shards, c, rounds = self._rounds(angle_range)
+        m0, m1 = shards[self.rank]
+        cur = torch.cuda.current_stream()
+        X.side.wait_stream(cur)          # y is ready on cur
+        for j in range(rounds):
+            slot = X.next_slot("bwd")
+            lo, hi = m0 + j * c, min(m0 + (j + 1) * c, m1)
+            X.wait_all(X.side, "read", slot)
+            if hi > lo:
+                with torch.cuda.stream(X.side):
+                    X.outbox[slot, :hi - lo].copy_(y[lo - m0:hi - m0])
+            X.record(X.side, "staged", slot)
+            X.barrier()
+            for s, (s0, s1) in enumerate(shards):
+                c0, c1 = s0 + j * c, min(s0 + (j + 1) * c, s1)
+                if c1 > c0 and z1 > z0:
+                    cur.wait_event(X.peer_ev[s]["staged"][slot])
+                    self.kernels.bwd_matched(
+                        X.outboxes[s][slot, :c1 - c0], self.geometry,
+                        (c0, c1), (z0, z1), out_slab)
+            X.record(cur, "read", slot)
+        cur.wait_stream(X.side)
         return out_slab
 
 

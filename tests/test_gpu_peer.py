@@ -1,0 +1,138 @@
+"""The sharded operators' peer-memory exchange (paper_1905_03748_b200/peer.py)
+on one GPU: 2 and 3 ranks (gloo for the host-side rendezvous) share
+cuda:0, so every "peer" inbox / outbox is CUDA-IPC-mapped memory of another
+process and the protocol -- IPC events, double-buffered slots, one host
+barrier per round -- runs for real.  The forward is checked bit for bit
+against the partials of every slab summed in rank order (what cs_sum_slices
+computes), the fused residual against w o (b - sum), the backward against
+the collective exchange (CS_EXCHANGE=nccl, here through gloo) and against
+single-process matched Atb of each slab."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+# 4 / 2 / 1 / 3 rounds of 2 views per shard at world 2: odd round counts
+# reuse the last slot in the next call's first round
+RANGES = ((0, 13), (3, 10), (5, 7), (0, 12), (2, 3))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _worker(rank, world, port, mode, q):
+    import sys
+    import torch
+    import torch.distributed as dist
+    for p in (ROOT, os.path.join(ROOT, "tests")):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["CS_EXCHANGE"] = mode
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from conftest import synth_geometry
+    from paper_1905_03748_b200 import kernels as K
+    from paper_1905_03748_b200.sharded import ShardedOperators, view_shards
+    dev = torch.device("cuda", 0)
+    n, na = 24, 13
+    g = synth_geometry(n, na, nu=28, nv=20)
+    ops = ShardedOperators(g, rank, world, round_views=2)   # 3+ rounds
+    z0, z1 = ops.slab
+    gen = torch.Generator(device=dev).manual_seed(5)
+    x = torch.rand((n, n, n), device=dev, generator=gen)
+    y = torch.randn((na, 20, 28), device=dev, generator=gen)
+    b = torch.randn((na, 20, 28), device=dev, generator=gen)
+    w = torch.rand((na, 20, 28), device=dev, generator=gen)
+    out = {}
+    for rep in range(2):                    # back-to-back calls reuse slots
+        for a0, a1 in RANGES:
+            s0, s1 = ops.shard((a0, a1))
+            fw = torch.empty((s1 - s0, 20, 28), device=dev)
+            ops.forward(x[z0:z1].contiguous(), fw, (a0, a1))
+            rs = torch.empty_like(fw)
+            ops.forward_residual(x[z0:z1].contiguous(), b[s0:s1], w[s0:s1],
+                                 rs, (a0, a1))
+            bw = torch.zeros((z1 - z0, n, n), device=dev)
+            ops.backward(y[s0:s1].contiguous(), bw, (a0, a1))
+            if rep == 1:   # rep 0 runs back to back: ranks drift apart
+                torch.cuda.synchronize()
+                out[(a0, a1)] = (fw.cpu().numpy(), rs.cpu().numpy(),
+                                 bw.cpu().numpy())
+    # references on this rank: every slab's partials summed in rank order,
+    # and each slab's matched Atb of the full range in one process
+    ref = {}
+    for a0, a1 in RANGES:
+        s0, s1 = view_shards(a0, a1, world)[rank]
+        tot = None
+        for q0, q1 in ops.slabs:
+            part = torch.zeros((s1 - s0, 20, 28), device=dev)
+            if q1 > q0 and s1 > s0:
+                K.fwd_interp(x[q0:q1].contiguous(), g, (s0, s1), (q0, q1),
+                             part)
+            tot = part if tot is None else tot + part
+        res = w[s0:s1] * (b[s0:s1] - tot)
+        bw = torch.zeros((z1 - z0, n, n), device=dev)
+        if z1 > z0:
+            K.bwd_matched(y[a0:a1].contiguous(), g, (a0, a1), (z0, z1), bw)
+        torch.cuda.synchronize()
+        ref[(a0, a1)] = (tot.cpu().numpy(), res.cpu().numpy(),
+                         bw.cpu().numpy())
+    q.put((rank, ops.exchange_mode, out, ref))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run(world, mode):
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        got = dict((r, (m, o, f)) for r, m, o, f in
+                   (q.get(timeout=600) for _ in range(world)))
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    assert all(p.exitcode == 0 for p in procs)
+    return got
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_exchange_matches_rank_order_sums(world):
+    peer = _run(world, "peer")
+    coll = _run(world, "nccl")
+    for r in range(world):
+        mode, out, ref = peer[r]
+        assert mode == "peer", "the peer exchange was not set up"
+        assert coll[r][0] == "collective"
+        for key, (fw, rs, bw) in out.items():
+            rfw, rrs, rbw = ref[key]
+            # forward + fused residual: the same kernels, summed in rank order
+            assert np.array_equal(fw, rfw), (r, key, _rel(fw, rfw))
+            assert np.array_equal(rs, rrs), (r, key, _rel(rs, rrs))
+            # backward: the same launches as the collective exchange (the
+            # matched kernel's fp32 flush order varies run to run)
+            cbw = coll[r][1][key][2]
+            assert _rel(bw, cbw) <= 1e-6, (r, key, _rel(bw, cbw))
+            assert _rel(bw, rbw) <= 1e-6, (r, key, _rel(bw, rbw))
+            # collective forward: identical kernels, sums in gloo's order
+            assert _rel(coll[r][1][key][0], rfw) <= 1e-6
