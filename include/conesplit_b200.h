@@ -96,6 +96,15 @@ int cs_bwd_matched(float* vol_acc, int nx, int ny, int nz, int z_lo,
                    int z_hi, const double* grid6, const double* geom, int n_a,
                    int n_u, int n_v, double step_max, const float* proj,
                    cs_stream_t stream);
+/* Run-to-run determinism of cs_bwd_matched (process-wide; default off, or
+ * CS_ST_DETERMINISTIC=1).  Off: CTAs add their (exact, integer) box sums
+ * into vol_acc with fp32 reductions, whose order -- and so the last bits of
+ * a voxel -- varies from run to run.  On: the contributions are rounded
+ * once to a launch-wide fixed point and summed as 64-bit integers in a
+ * slab-sized scratch accumulator (8 B per voxel, from CUDA's stream-ordered
+ * pool), then added into vol_acc: bit-identical results every run, as the
+ * reference's fp64 host accumulation is (_kernels.py:278-337). */
+int cs_set_deterministic(int on);
 
 /* Voxel-driven FDK-weighted backprojection, accumulated into slab
  * vol_acc = grid slices [z_lo, z_lo + n_slab).

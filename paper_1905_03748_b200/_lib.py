@@ -67,6 +67,7 @@ SYMBOLS: dict[str, list] = {
     "cs_weighted_residual": [P, P, P, L, P],
     "cs_fill": [P, ctypes.c_float, L, P],
     "cs_sum_slices": [P, I, L, L, P, P, P, P],
+    "cs_set_deterministic": [I],
     "cs_peer_enable": [I],
 }
 

@@ -93,6 +93,25 @@ __device__ __forceinline__ void st_red4(float* p, float a, float b, float c,
                : "memory");
 }
 
+// Deterministic matched Atb (cs_set_deterministic / CS_ST_DETERMINISTIC=1):
+// every contribution that would be an fp32 red into the volume -- a CTA's
+// flushed box voxel (itself an exact integer sum: the box is
+// order-independent) or a global-path tap -- is rounded once to a launch-wide
+// fixed point S = 2^k and added as a 64-bit integer (RED.E.ADD.64: integer
+// adds are associative, so the total does not depend on the order in which
+// CTAs finish); one pass adds acc / S into the fp32 volume at the end.  S is
+// the largest power of two with n_a * max|proj| * step_max * taps * S <
+// 2^62 (taps = samples of all rays in one voxel's support per view), from
+// the launch's |proj| maximum on the device.
+// (S is read from device memory at each use -- the launch computed it --
+// so the production path keeps no register for it.)
+__device__ __forceinline__ void det_add(long long* p, float v,
+                                        const double* S) {
+  if (v != 0.f)
+    atomicAdd(reinterpret_cast<unsigned long long*>(p),
+              (unsigned long long)__double2ll_rn((double)v * __ldg(S)));
+}
+
 // Precise boxes (matched only, chosen per chunk, CTA-uniform): every voxel
 // holds an int2 (hi, lo): hi sums the taps rounded to the CTA's unit
 // (scale = fx_budget / max tap), lo sums their exact rounding residuals
@@ -119,7 +138,8 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
                   const float* __restrict__ rb, const float* __restrict__ rw,
                   int box_cap, float fx_budget, int vec_ok, int lane_stride,
                   int prec_mode, float prec_fp, int edge, float lo_scale,
-                  int tpad) {
+                  int tpad, long long* __restrict__ dacc,
+                  const double* __restrict__ dscale) {
   constexpr int T = 1 - M;
   extern __shared__ float4 st_box4[];
   float* st_box = reinterpret_cast<float*>(st_box4);
@@ -304,6 +324,8 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
             const size_t gi = (size_t)(zi - z_lo) * plane + (size_t)yi * nx + xi;
             if (OP == OP_FWD)
               acc = fmaf(w, __ldg(vol_in + gi), acc);
+            else if (dacc)
+              det_add(dacc + gi, val * (float)r.step * w, dscale);
             else
               atomicAdd(vol_acc + gi, val * (float)r.step * w);
           }
@@ -621,6 +643,8 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
                     (size_t)(zi - z_lo) * plane + (size_t)yi * nx + xi;
                 if (OP == OP_FWD)
                   acc = fmaf(w, __ldg(vol_in + gi), acc);
+                else if (dacc)
+                  det_add(dacc + gi, val * (float)r.step * w, dscale);
                 else
                   atomicAdd(vol_acc + gi, val * (float)r.step * w);
               }
@@ -741,7 +765,13 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
             f0 = (float)q0 * inv_scale; f1 = (float)q1 * inv_scale;
             f2 = (float)q2 * inv_scale; f3 = (float)q3 * inv_scale;
           }
-          if (vec) {
+          if (dacc) {
+            const float f[4] = {f0, f1, f2, f3};
+            long long* dp = dacc + (gp - vol_acc);
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+              if (gx + j >= 0 && gx + j < nx) det_add(dp + j, f[j], dscale);
+          } else if (vec) {
             st_red4(gp, f0, f1, f2, f3);
           } else {
             const float f[4] = {f0, f1, f2, f3};
@@ -864,6 +894,50 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Deterministic matched Atb (see det_add): the launch's max |proj| (float
+// bits of non-negative values order like unsigned ints), and the final
+// vol += acc / S.
+__global__ void __launch_bounds__(256)
+    abs_max_kernel(const float* __restrict__ x, size_t n,
+                   unsigned* __restrict__ out) {
+  float m = 0.f;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(x[i]));
+  for (int o = 16; o > 0; o >>= 1)
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
+}
+
+__global__ void det_scale_kernel(const unsigned* __restrict__ gmax_bits,
+                                 double det_c, double* __restrict__ S) {
+  const float g = __uint_as_float(*gmax_bits);
+  *S = g > 0.f ? exp2(floor(log2(det_c / (double)g))) : 0.0;
+}
+
+__global__ void __launch_bounds__(256)
+    det_finish_kernel(float* __restrict__ vol, const long long* __restrict__ acc,
+                      size_t n, const double* __restrict__ dscale) {
+  const double S = *dscale;
+  if (S == 0.0) return;
+  const double inv = 1.0 / S;   // a power of two: exact
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const long long q = acc[i];
+    if (q) vol[i] += (float)((double)q * inv);
+  }
+}
+
+static int g_deterministic = -1;   // -1: CS_ST_DETERMINISTIC decides
+
+static bool deterministic_matched() {
+  if (g_deterministic < 0) {
+    const char* k = getenv("CS_ST_DETERMINISTIC");
+    g_deterministic = (k && k[0] == '1') ? 1 : 0;
+  }
+  return g_deterministic == 1;
+}
+
 // Launch one staged pass over n_a views (OP_FWD: Ax into out with MODE
 // epilogue; OP_BWD: matched Atb into vol_acc).
 template <int OP, int MODE>
@@ -905,7 +979,8 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   // below; knob CS_ST_TRANSPOSE=0 disables).
   bool use_t = false;
   const size_t slab_bytes = (size_t)(z_hi - z_lo) * nx * ny * sizeof(float);
-  if (OP == OP_BWD && nxm > 0) {
+  const bool det = OP == OP_BWD && deterministic_matched();
+  if (OP == OP_BWD && nxm > 0 && !det) {
     static const char* tk = getenv("CS_ST_TRANSPOSE");
     size_t free_b = 0, total_b = 0;
     use_t = !(tk && tk[0] == '0') &&
@@ -1073,6 +1148,44 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   // spreads a warp's REDs over 32 rows: 34.2 vs 24.3 ms per 45 views at
   // 512^3 (profiles/ncu_r02w.md).  Needs a slab-sized buffer: used when the
   // device has room for it (knob CS_ST_TRANSPOSE=0 disables).
+  // deterministic mode: a slab-sized int64 accumulator (x-major views in
+  // their own frame, so one accumulator serves both classes)
+  long long* dacc = nullptr;
+  unsigned* dgmax = nullptr;   // [0]: max |proj| bits; [2..3]: S (double)
+  double* dscale = nullptr;
+  double det_c = 0.0;
+  if (det) {
+    const size_t nvox = (size_t)(z_hi - z_lo) * nx * ny;
+    double fp = fmax(min_pixel_footprint(grid6, nx, ny, nz, geom, n_a, n_u,
+                                         n_v), 1e-3);
+    const double vmax = fmax(grid6[3], fmax(grid6[4], grid6[5]));
+    const double taps_all = (2.0 / fp + 1.0) * (2.0 / fp + 1.0) *
+                            (2.0 * vmax / (0.5 * step_max) + 1.0);
+    det_c = ldexp(1.0, 62) / (2.0 * n_a * step_max * taps_all);
+    cudaError_t ed = cudaMallocAsync((void**)&dacc, nvox * sizeof(long long),
+                                     s);
+    if (ed == cudaSuccess)
+      ed = cudaMallocAsync((void**)&dgmax, 4 * sizeof(unsigned), s);
+    if (ed == cudaSuccess)
+      ed = cudaMemsetAsync(dacc, 0, nvox * sizeof(long long), s);
+    if (ed == cudaSuccess) ed = cudaMemsetAsync(dgmax, 0, sizeof(unsigned), s);
+    if (ed == cudaSuccess) {
+      dscale = reinterpret_cast<double*>(dgmax + 2);
+      abs_max_kernel<<<num_sms() * 4, 256, 0, s>>>(
+          proj_in, (size_t)n_a * n_u * n_v, dgmax);
+      CS_COUNT_LAUNCH();
+      det_scale_kernel<<<1, 1, 0, s>>>(dgmax, det_c, dscale);
+      CS_COUNT_LAUNCH();
+      ed = cudaGetLastError();
+    }
+    if (ed != cudaSuccess) {
+      if (dacc) cudaFreeAsync(dacc, s);
+      if (dgmax) cudaFreeAsync(dgmax, s);
+      cudaFreeAsync(ids, s);
+      release_geometry(dgeom, s);
+      CS_CHECK_CUDA(ed);
+    }
+  }
   bool transposed = false;
   if (use_t && rows(0) > 0) {
     double* geom_t = (double*)malloc(sizeof(double) * 12 * (size_t)n_a);
@@ -1100,7 +1213,8 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
       k1<<<grid_of(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
           vol_in, acc_t, dgeom_t, ids, GT, step_max, z_lo, z_hi, n_u, n_v,
           band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_t,
-          lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad);
+          lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad, nullptr,
+          nullptr);
       CS_COUNT_LAUNCH();
       const dim3 tg((ny + 31) / 32, (nx + 31) / 32, z_hi - z_lo);
       transpose_add_kernel<<<tg, dim3(32, 8), 0, s>>>(vol_acc, acc_t, nx,
@@ -1127,15 +1241,22 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     k0<<<grid_of(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids, G, step_max, z_lo, z_hi, n_u, n_v,
         band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_ok,
-        lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad);
+        lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad, dacc, dscale);
     CS_COUNT_LAUNCH();
   }
   if (nall > nxm && rows(1) > 0) {
     k1<<<grid_of(gx, rows(1), nall - nxm), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids + nxm, G, step_max, z_lo, z_hi, n_u, n_v,
         band[1][0], band[1][1], out, proj_in, rb, rw, cap, budget, vec_ok,
-        lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad);
+        lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad, dacc, dscale);
     CS_COUNT_LAUNCH();
+  }
+  if (det) {
+    det_finish_kernel<<<num_sms() * 8, 256, 0, s>>>(
+        vol_acc, dacc, (size_t)(z_hi - z_lo) * nx * ny, dscale);
+    CS_COUNT_LAUNCH();
+    cudaFreeAsync(dacc, s);
+    cudaFreeAsync(dgmax, s);
   }
   e = cudaGetLastError();
   cudaFreeAsync(ids, s);
@@ -1167,3 +1288,8 @@ template int launch_staged<OP_BWD, 0>(const float*, float*, int, int, int,
                                       const float*, cudaStream_t);
 
 }  // namespace cs
+
+extern "C" int cs_set_deterministic(int on) {
+  cs::g_deterministic = on ? 1 : 0;
+  return CS_OK;
+}

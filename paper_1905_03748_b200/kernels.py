@@ -149,6 +149,12 @@ def bwd_matched(proj: torch.Tensor, geometry: ScanGeometry, angle_range,
     return vol_acc
 
 
+def set_deterministic(on: bool) -> None:
+    """Bit-reproducible matched Atb (int64 fixed-point accumulation; see
+    cs_set_deterministic) for every later bwd_matched in this process."""
+    check(lib().cs_set_deterministic(int(bool(on))))
+
+
 def bwd_fdk(proj: torch.Tensor, geometry: ScanGeometry, angle_range,
             slab_range, vol_acc: torch.Tensor, stream=None) -> torch.Tensor:
     """K3: vol_acc += FDK-weighted backprojection (dso/U)^2 * bilinear."""
