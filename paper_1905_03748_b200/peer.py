@@ -33,10 +33,14 @@ barrier -- is waited on by the slot's next user only after the barrier of
 the round in between, which no rank passes before recording it: every wait
 resolves to the record of the intended round.
 
-The mapping is validated at set-up (each rank's fill kernel stores a marker
-into every peer's inbox, the owner checks it); ``PeerExchange.create``
-returns None when CUDA IPC or P2P is unavailable, and the operators keep
-NCCL's collectives.
+The mapping is validated at set-up through the launch paths the operators
+use: each rank's fill kernel stores a marker row and its Ax kernel (the
+v-band memset included) a probe view of a small volume into every peer's
+inbox, and its matched kernel backprojects every peer's outbox pattern; the
+owners / readers compare with the same launches on local memory.
+``PeerExchange.create`` returns None on every rank when CUDA IPC or P2P is
+unavailable or a probe disagrees anywhere, and the operators keep NCCL's
+collectives.
 """
 
 from __future__ import annotations
@@ -63,8 +67,10 @@ class PeerExchange:
     KINDS = ("written", "consumed", "staged", "read")
 
     def __init__(self, rank: int, world: int, device: torch.device,
-                 round_views: int, sheet: tuple[int, int], group=None):
+                 round_views: int, sheet: tuple[int, int], group=None,
+                 geometry=None):
         self.rank, self.world, self.c = rank, world, round_views
+        self.probe = None if geometry is None else _probe_geometry(geometry)
         self.device = device
         self.group = group
         n_v, n_u = sheet
@@ -85,7 +91,8 @@ class PeerExchange:
 
     # ---------------------------------------------------------- set-up
     @classmethod
-    def create(cls, rank, world, device, round_views, sheet, group=None):
+    def create(cls, rank, world, device, round_views, sheet, group=None,
+               geometry=None):
         """Collective over the ranks; None (on every rank) when the peer
         path is unavailable on any of them.  Each stage ends in an
         all-gather, so a rank that fails still takes part in every
@@ -97,7 +104,8 @@ class PeerExchange:
 
         ex, mine = None, None
         try:
-            ex = cls(rank, world, device, round_views, sheet, group)
+            ex = cls(rank, world, device, round_views, sheet, group,
+                     geometry)
             mine = ex._handles()
         except Exception as e:  # noqa: BLE001 - reported, then agreed on
             warnings.warn(f"peer exchange unavailable on rank {rank}: {e!r}")
@@ -162,26 +170,66 @@ class PeerExchange:
     def _marker(self, writer: int, owner: int) -> float:
         return float(1 + writer * self.world + owner)
 
+    def _pattern(self, rank: int) -> float:
+        return 0.25 * (rank + 1)
+
     def _mark_peers(self):
-        """Set-up check, part 1: this rank's fill kernel stores a marker row
-        into its slot of every owner's inbox (peer stores)."""
+        """Set-up check, part 1 (peer stores): the fill kernel writes a
+        marker row into this rank's slot of every owner's inbox (slot 0),
+        the Ax kernel a probe view (slot 1); the outbox gets this rank's
+        pattern for the readers."""
         with torch.cuda.device(self.device):
             cur = torch.cuda.current_stream()
             for s in range(self.world):
                 K.fill(self.inboxes[s][0, self.rank, 0, 0],
                        self._marker(self.rank, s))
+            if self.probe is not None:
+                g, vol = self.probe, self._probe_volume()
+                for s in range(self.world):
+                    K.fwd_interp(vol, g, (0, 1), (0, vol.shape[0]),
+                                 self.inboxes[s][1, self.rank, :1])
+            K.fill(self.outbox[0, :1], self._pattern(self.rank))
             self.ev["written"][0].record(cur)
+            self.ev["staged"][0].record(cur)
+
+    def _probe_volume(self):
+        n = self.probe.voxel_grid.n_x
+        i = torch.arange(n ** 3, dtype=torch.float32, device=self.device)
+        return (1.0 + (i % 7) / 7.0).reshape(n, n, n)
 
     def _check_marks(self) -> bool:
-        """Part 2 (after a barrier): the owner reads every writer's row."""
+        """Part 2 (after a barrier): the owner reads every writer's marker
+        and probe view (bit-identical to its own launch of the same Ax),
+        and backprojects every peer's outbox with the matched kernel
+        (against the same launch on a local copy of the pattern)."""
         with torch.cuda.device(self.device):
             cur = torch.cuda.current_stream()
             self.wait_all(cur, "written", 0)
+            self.wait_all(cur, "staged", 0)
             got = self.inbox[0, :, 0, 0].cpu()
+            ok = True
+            if self.probe is not None:
+                g, vol = self.probe, self._probe_volume()
+                nz = vol.shape[0]
+                mine = torch.empty_like(self.inbox[1, 0, :1])
+                K.fwd_interp(vol, g, (0, 1), (0, nz), mine)
+                ok = bool((self.inbox[1, :, :1] == mine).all().item())
+                for s in range(self.world):
+                    far = torch.zeros_like(vol)
+                    K.bwd_matched(self.outboxes[s][0, :1], g, (0, 1),
+                                  (0, nz), far)
+                    near = torch.zeros_like(vol)
+                    K.bwd_matched(K.fill(torch.empty_like(mine),
+                                         self._pattern(s)),
+                                  g, (0, 1), (0, nz), near)
+                    err = (far - near).norm() / near.norm().clamp_min(1e-30)
+                    ok = ok and float(err.item()) <= 1e-6
             self.ev["consumed"][0].record(cur)
+            self.ev["consumed"][1].record(cur)
+            self.ev["read"][0].record(cur)
         want = torch.tensor([self._marker(s, self.rank)
                              for s in range(self.world)])
-        return bool((got == want[:, None]).all())
+        return ok and bool((got == want[:, None]).all())
 
     def barrier(self):
         """Host-only rendezvous (no device synchronisation)."""
@@ -204,3 +252,15 @@ class PeerExchange:
 
     def record(self, stream, kind: str, slot: int):
         self.ev[kind][slot].record(stream)
+
+
+def _probe_geometry(geometry):
+    """One view of the operators' geometry on an 8^3 grid spanning the
+    same field of view (every detector row of the probe sees the cone)."""
+    from .geometry import ScanGeometry, VoxelGrid
+    g = geometry.voxel_grid
+    n = 8
+    vs = tuple(float(v) * c / n for v, c in zip(g.voxel_size, g.counts))
+    return ScanGeometry(geometry.dso, geometry.dsd, (float(geometry.angles[0]),),
+                        VoxelGrid(n, n, n, vs, tuple(g.origin_offset)),
+                        geometry.detector)

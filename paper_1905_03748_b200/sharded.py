@@ -204,7 +204,7 @@ class ShardedOperators:
         det = self.geometry.detector
         self._peer = PeerExchange.create(
             self.rank, self.world, like.device, self.round_views,
-            (det.n_v, det.n_u), group)
+            (det.n_v, det.n_u), group, self.geometry)
         return self._peer
 
     @property
