@@ -152,6 +152,10 @@ class _CudaKernels:
 
 # --------------------------------------------------------------- operators
 
+_EXCHANGES: dict = {}     # peer exchanges by (process group, rank, shape)
+_HOST_GROUPS: dict = {}   # gloo group per NCCL process group (host barrier)
+
+
 @dataclass
 class ShardedOperators:
     """A / A^T with the volume slab-sharded and the views angle-sharded.
@@ -200,11 +204,24 @@ class ShardedOperators:
         self._peer_tried = True
         if not peer_mode_requested():
             return None
-        group = None if not _nccl() else dist.new_group(backend="gloo")
+        # one exchange (buffers, mappings, events, gloo group) per process
+        # group and shape, shared by every ShardedOperators the loops
+        # create: the ranks reach this point in the same order
         det = self.geometry.detector
-        self._peer = PeerExchange.create(
-            self.rank, self.world, like.device, self.round_views,
-            (det.n_v, det.n_u), group, self.geometry)
+        pg = dist.distributed_c10d._get_default_group()
+        key = (id(pg), self.rank, self.world, like.device.index,
+               self.round_views, det.n_v, det.n_u)
+        if key not in _EXCHANGES:
+            if _nccl():
+                if id(pg) not in _HOST_GROUPS:
+                    _HOST_GROUPS[id(pg)] = dist.new_group(backend="gloo")
+                group = _HOST_GROUPS[id(pg)]
+            else:
+                group = None
+            _EXCHANGES[key] = PeerExchange.create(
+                self.rank, self.world, like.device, self.round_views,
+                (det.n_v, det.n_u), group, self.geometry)
+        self._peer = _EXCHANGES[key]
         return self._peer
 
     @property

@@ -82,6 +82,10 @@ def _worker(rank, world, port, mode, q):
         torch.cuda.synchronize()
         ref[(a0, a1)] = (tot.cpu().numpy(), res.cpu().numpy(),
                          bw.cpu().numpy())
+    # a second operator object (the loops create one per call) shares the
+    # process's exchange: no second set of buffers, mappings or groups
+    ops2 = ShardedOperators(g, rank, world, round_views=2)
+    assert ops2.exchange(x) is ops.exchange(x)
     q.put((rank, ops.exchange_mode, out, ref))
     dist.barrier()
     dist.destroy_process_group()
