@@ -23,4 +23,7 @@ run "memcheck, Ax sub-slabs (CS_TEX_MAX_MB=0.03: 20-plane slab in 10-plane piece
 run "memcheck, z-layered Ax" memcheck CS_FWD_MLAYER=0
 run "racecheck, matched x-major views in their own frame (CS_ST_TRANSPOSE=0)" racecheck CS_ST_TRANSPOSE=0
 run "memcheck, matched x-major views in their own frame (CS_ST_TRANSPOSE=0)" memcheck CS_ST_TRANSPOSE=0
+run "memcheck, deterministic matched (CS_ST_DETERMINISTIC=1)" memcheck CS_ST_DETERMINISTIC=1
+run "racecheck, deterministic matched (CS_ST_DETERMINISTIC=1)" racecheck CS_ST_DETERMINISTIC=1
+run "memcheck, deterministic matched with 2 KB boxes (global path)" memcheck CS_ST_DETERMINISTIC=1 CS_STAGED_SMEM_KB=2
 } > $out
