@@ -141,6 +141,10 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
                   int tpad, long long* __restrict__ dacc,
                   const double* __restrict__ dscale) {
   constexpr int T = 1 - M;
+  // matched in deterministic mode is the MODE = 3 instantiation (MODE is
+  // otherwise an Ax epilogue selector): the default kernels carry no trace
+  // of it
+  constexpr bool DET = OP == OP_BWD && MODE == 3;
   extern __shared__ float4 st_box4[];
   float* st_box = reinterpret_cast<float*>(st_box4);
   int* box_i = reinterpret_cast<int*>(st_box4);
@@ -324,7 +328,7 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
             const size_t gi = (size_t)(zi - z_lo) * plane + (size_t)yi * nx + xi;
             if (OP == OP_FWD)
               acc = fmaf(w, __ldg(vol_in + gi), acc);
-            else if (dacc)
+            else if (DET)
               det_add(dacc + gi, val * (float)r.step * w, dscale);
             else
               atomicAdd(vol_acc + gi, val * (float)r.step * w);
@@ -643,7 +647,7 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
                     (size_t)(zi - z_lo) * plane + (size_t)yi * nx + xi;
                 if (OP == OP_FWD)
                   acc = fmaf(w, __ldg(vol_in + gi), acc);
-                else if (dacc)
+                else if (DET)
                   det_add(dacc + gi, val * (float)r.step * w, dscale);
                 else
                   atomicAdd(vol_acc + gi, val * (float)r.step * w);
@@ -765,7 +769,7 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
             f0 = (float)q0 * inv_scale; f1 = (float)q1 * inv_scale;
             f2 = (float)q2 * inv_scale; f3 = (float)q3 * inv_scale;
           }
-          if (dacc) {
+          if (DET) {
             const float f[4] = {f0, f1, f2, f3};
             long long* dp = dacc + (gp - vol_acc);
 #pragma unroll
@@ -1119,10 +1123,20 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   auto grid_of = [&](unsigned tu, unsigned tv, unsigned nv) {
     return (OP == OP_BWD && CS_ST_VIEWFAST) ? dim3(nv, tu, tv) : dim3(tu, tv, nv);
   };
-  auto k0 = deep ? staged_kernel<OP, 0, MODE, 3, ST_S_DEEP>
-            : four ? staged_kernel<OP, 0, MODE, 4> : staged_kernel<OP, 0, MODE, 3>;
-  auto k1 = deep ? staged_kernel<OP, 1, MODE, 3, ST_S_DEEP>
-            : four ? staged_kernel<OP, 1, MODE, 4> : staged_kernel<OP, 1, MODE, 3>;
+  // DM: the deterministic matched instantiation (MODE 3; == MODE for Ax)
+  constexpr int DM = OP == OP_BWD ? 3 : MODE;
+  auto k0 = deep ? (det ? staged_kernel<OP, 0, DM, 3, ST_S_DEEP>
+                        : staged_kernel<OP, 0, MODE, 3, ST_S_DEEP>)
+            : four ? (det ? staged_kernel<OP, 0, DM, 4>
+                          : staged_kernel<OP, 0, MODE, 4>)
+                   : (det ? staged_kernel<OP, 0, DM, 3>
+                          : staged_kernel<OP, 0, MODE, 3>);
+  auto k1 = deep ? (det ? staged_kernel<OP, 1, DM, 3, ST_S_DEEP>
+                        : staged_kernel<OP, 1, MODE, 3, ST_S_DEEP>)
+            : four ? (det ? staged_kernel<OP, 1, DM, 4>
+                          : staged_kernel<OP, 1, MODE, 4>)
+                   : (det ? staged_kernel<OP, 1, DM, 3>
+                          : staged_kernel<OP, 1, MODE, 3>);
   // the dynamic shared-memory opt-in is per device: set it once on each
   // (the executor drives several GPUs from one process)
   static std::atomic<unsigned long long> attr_done{0};
@@ -1133,7 +1147,11 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     for (auto k : {staged_kernel<OP, 0, MODE, 3>, staged_kernel<OP, 1, MODE, 3>,
                    staged_kernel<OP, 0, MODE, 4>, staged_kernel<OP, 1, MODE, 4>,
                    staged_kernel<OP, 0, MODE, 3, ST_S_DEEP>,
-                   staged_kernel<OP, 1, MODE, 3, ST_S_DEEP>})
+                   staged_kernel<OP, 1, MODE, 3, ST_S_DEEP>,
+                   staged_kernel<OP, 0, DM, 3>, staged_kernel<OP, 1, DM, 3>,
+                   staged_kernel<OP, 0, DM, 4>, staged_kernel<OP, 1, DM, 4>,
+                   staged_kernel<OP, 0, DM, 3, ST_S_DEEP>,
+                   staged_kernel<OP, 1, DM, 3, ST_S_DEEP>})
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            200 * 1024);
     attr_done.fetch_or(bit);
