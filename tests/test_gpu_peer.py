@@ -23,7 +23,7 @@ RANGES = ((0, 13), (3, 10), (5, 7), (0, 12), (2, 3))
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _worker(rank, world, port, mode, q):
+def _worker(rank, world, port, mode, q, nu=28, nv=20):
     import sys
     import torch
     import torch.distributed as dist
@@ -40,19 +40,19 @@ def _worker(rank, world, port, mode, q):
     from paper_1905_03748_b200.sharded import ShardedOperators, view_shards
     dev = torch.device("cuda", 0)
     n, na = 24, 13
-    g = synth_geometry(n, na, nu=28, nv=20)
+    g = synth_geometry(n, na, nu=nu, nv=nv)
     ops = ShardedOperators(g, rank, world, round_views=2)   # 3+ rounds
     z0, z1 = ops.slab
     gen = torch.Generator(device=dev).manual_seed(5)
     x = torch.rand((n, n, n), device=dev, generator=gen)
-    y = torch.randn((na, 20, 28), device=dev, generator=gen)
-    b = torch.randn((na, 20, 28), device=dev, generator=gen)
-    w = torch.rand((na, 20, 28), device=dev, generator=gen)
+    y = torch.randn((na, nv, nu), device=dev, generator=gen)
+    b = torch.randn((na, nv, nu), device=dev, generator=gen)
+    w = torch.rand((na, nv, nu), device=dev, generator=gen)
     out = {}
     for rep in range(2):                    # back-to-back calls reuse slots
         for a0, a1 in RANGES:
             s0, s1 = ops.shard((a0, a1))
-            fw = torch.empty((s1 - s0, 20, 28), device=dev)
+            fw = torch.empty((s1 - s0, nv, nu), device=dev)
             ops.forward(x[z0:z1].contiguous(), fw, (a0, a1))
             rs = torch.empty_like(fw)
             ops.forward_residual(x[z0:z1].contiguous(), b[s0:s1], w[s0:s1],
@@ -70,7 +70,7 @@ def _worker(rank, world, port, mode, q):
         s0, s1 = view_shards(a0, a1, world)[rank]
         tot = None
         for q0, q1 in ops.slabs:
-            part = torch.zeros((s1 - s0, 20, 28), device=dev)
+            part = torch.zeros((s1 - s0, nv, nu), device=dev)
             if q1 > q0 and s1 > s0:
                 K.fwd_interp(x[q0:q1].contiguous(), g, (s0, s1), (q0, q1),
                              part)
@@ -91,7 +91,7 @@ def _worker(rank, world, port, mode, q):
     dist.destroy_process_group()
 
 
-def _run(world, mode):
+def _run(world, mode, nu=28, nv=20):
     import socket
     import torch.multiprocessing as mp
     s = socket.socket()
@@ -100,7 +100,8 @@ def _run(world, mode):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q))
+    procs = [ctx.Process(target=_worker,
+                         args=(r, world, port, mode, q, nu, nv))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -120,10 +121,12 @@ def _rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_peer_exchange_matches_rank_order_sums(world):
-    peer = _run(world, "peer")
-    coll = _run(world, "nccl")
+@pytest.mark.parametrize("world,nu,nv", [(2, 28, 20), (3, 28, 20),
+                                         (2, 27, 19)])
+def test_peer_exchange_matches_rank_order_sums(world, nu, nv):
+    """(27 x 19 sheets: the owners' sum takes cs_sum_slices' scalar path.)"""
+    peer = _run(world, "peer", nu, nv)
+    coll = _run(world, "nccl", nu, nv)
     for r in range(world):
         mode, out, ref = peer[r]
         assert mode == "peer", "the peer exchange was not set up"
