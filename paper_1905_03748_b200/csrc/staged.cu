@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
                   int box_cap, float fx_budget, int vec_ok, int lane_stride,
                   int prec_mode, float prec_fp, int edge, float lo_scale,
                   int tpad, long long* __restrict__ dacc,
-                  const double* __restrict__ dscale) {
+                  const double* __restrict__ dscale, int vpair, int n_ids) {
   constexpr int T = 1 - M;
   // matched in deterministic mode is the MODE = 3 instantiation (MODE is
   // otherwise an Ax epilogue selector): the default kernels carry no trace
@@ -181,12 +181,20 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
   const int bidx = vf ? blockIdx.y : blockIdx.x;   // detector u tile
   const int bidy = vf ? blockIdx.z : blockIdx.y;   // detector v tile
   const int bidv = vf ? blockIdx.x : blockIdx.z;   // view
+  // view pairs (matched, lane stride 1): warps 0-3 take 4 detector rows of
+  // view 2 bidv, warps 4-7 the same rows of view 2 bidv + 1 -- neighbouring
+  // angles whose rays cross nearly the same voxels, so one box of about half
+  // the z extent serves 256 rays and the flush per ray roughly halves
+  const bool pr = OP == OP_BWD && vpair;
+  const int wv = pr ? (warp & 3) : warp;
+  const int tv_rows = pr ? ST_TV / 2 : ST_TV / lane_stride;
+  const int vi = pr ? 2 * bidv + (warp >> 2) : bidv;
   const int u = bidx * (ST_TU * lane_stride) + lane * lane_stride +
-                (warp & (lane_stride - 1));
-  const int v = v_base + bidy * (ST_TV / lane_stride) +
-                warp / lane_stride;
-  const int a = view_ids[bidv];
-  const bool valid = u < n_u && v < v_end;
+                (wv & (lane_stride - 1));
+  const int v = v_base + bidy * tv_rows + (pr ? wv : warp / lane_stride);
+  const bool has_view = vi < n_ids;
+  const int a = view_ids[has_view ? vi : 0];
+  const bool valid = has_view && u < n_u && v < v_end;
   const int nx = G.n[0], ny = G.n[1];
   const size_t plane = (size_t)nx * ny;
   const size_t pix = ((size_t)a * n_v + v) * n_u + u;
@@ -290,7 +298,7 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
   if (OP == OP_BWD && threadIdx.x == 0) {
     bool pc = prec_mode == 1;
     if (prec_mode == 0) {
-      const int tu = ST_TU * lane_stride, tv = ST_TV / lane_stride;
+      const int tu = ST_TU * lane_stride, tv = tv_rows;
       const int u_first = bidx * tu, v_first = v_base + bidy * tv;
       pc = u_first < edge || u_first + tu > n_u - edge ||
            v_first < edge || v_first + tv > n_v - edge;
@@ -1102,10 +1110,21 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   static const char* tp_knob = getenv("CS_ST_TPAD");
   const int tpad = OP == OP_BWD ? (tp_knob ? atoi(tp_knob) : 31) : 0;
   const unsigned gx = (n_u + ST_TU * lane_stride - 1) / (ST_TU * lane_stride);
+  // matched view pairs per CTA (see the kernel; A/B knob CS_ST_PAIR=1, off
+  // by default: dense 180 views at 256^3 / 512^3 / 1024^3: 224.4 / 260.4 /
+  // 274.7 vs 216.7 / 263.6 / 282.0 GUPS -- the shared box shrinks only to
+  // ~0.7x (the views' footprints are shifted, the rays' z drift over a
+  // 14-plane chunk remains), profiles/ab_matched_view_pairs_r02bp.jsonl);
+  // with lane stride 1 and without the few-view ray-gap rule (its source
+  // position is per view)
+  static const char* pair_knob = getenv("CS_ST_PAIR");
+  const int vpair = OP == OP_BWD && lane_stride == 1 && prec_fp >= 1e29f &&
+                    pair_knob && pair_knob[0] == '1';
   auto rows = [&](int c) {
-    const int rv = ST_TV / lane_stride;
+    const int rv = vpair ? ST_TV / 2 : ST_TV / lane_stride;
     return (unsigned)((band[c][1] - band[c][0] + rv - 1) / rv);
   };
+  auto nviews = [&](int n) { return (unsigned)(vpair ? (n + 1) / 2 : n); };
   // matched chunk depth: 14 planes with 3 CTAs x 72 KB boxes for planes of
   // >= 512^2 voxels (512^3: 261.6 vs 249.1 GUPS dense for 8 planes at 4 x 54
   // KB, 1024^3: 271.6 vs 262.1, 2048^3 x 32 views: 260.5 vs 263.9), else 8
@@ -1228,11 +1247,11 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
       e2 = cudaMemsetAsync(acc_t, 0, slab_bytes, s);
     if (!rc && e2 == cudaSuccess) {
       const int vec_t = (ny % 4 == 0);
-      k1<<<grid_of(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
+      k1<<<grid_of(gx, rows(0), nviews(nxm)), ST_THREADS, smem, s>>>(
           vol_in, acc_t, dgeom_t, ids, GT, step_max, z_lo, z_hi, n_u, n_v,
           band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_t,
           lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad, nullptr,
-          nullptr);
+          nullptr, vpair, nxm);
       CS_COUNT_LAUNCH();
       const dim3 tg((ny + 31) / 32, (nx + 31) / 32, z_hi - z_lo);
       transpose_add_kernel<<<tg, dim3(32, 8), 0, s>>>(vol_acc, acc_t, nx,
@@ -1256,17 +1275,19 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     }
   }
   if (!transposed && nxm > 0 && rows(0) > 0) {
-    k0<<<grid_of(gx, rows(0), nxm), ST_THREADS, smem, s>>>(
+    k0<<<grid_of(gx, rows(0), nviews(nxm)), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids, G, step_max, z_lo, z_hi, n_u, n_v,
         band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_ok,
-        lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad, dacc, dscale);
+        lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad, dacc, dscale,
+        vpair, nxm);
     CS_COUNT_LAUNCH();
   }
   if (nall > nxm && rows(1) > 0) {
-    k1<<<grid_of(gx, rows(1), nall - nxm), ST_THREADS, smem, s>>>(
+    k1<<<grid_of(gx, rows(1), nviews(nall - nxm)), ST_THREADS, smem, s>>>(
         vol_in, vol_acc, dgeom, ids + nxm, G, step_max, z_lo, z_hi, n_u, n_v,
         band[1][0], band[1][1], out, proj_in, rb, rw, cap, budget, vec_ok,
-        lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad, dacc, dscale);
+        lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad, dacc, dscale,
+        vpair, nall - nxm);
     CS_COUNT_LAUNCH();
   }
   if (det) {
