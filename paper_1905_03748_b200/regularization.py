@@ -252,69 +252,138 @@ def _h2d(a: np.ndarray) -> torch.Tensor:
         torch.device("cuda", torch.cuda.current_device()))
 
 
+def _stream_windows(slabs: list[HaloSlab], n_z: int) -> list[HaloSlab] | None:
+    """ExactGlobal streaming windows: each planned core cut into pieces so
+    that TWO (window, gradient) buffer pairs fit where the plan budgeted
+    one (regularization.py:197-210), for double buffering.  ExactGlobal
+    results do not depend on the partition (every core plane sees a full
+    halo; the norm is global).  None when the pieces would be thinner than
+    the halo (then one pair is streamed at a time)."""
+    out = []
+    for s in slabs:
+        z0, z1 = s.core_range
+        d = s.halo_depth
+        w = s.window[1] - s.window[0]
+        piece = w // 2 - 2 * d
+        if piece < max(8, d):
+            return None
+        k = -(-(z1 - z0) // piece)           # even pieces of <= piece
+        for j in range(k):
+            a, b = z0 + (z1 - z0) * j // k, z0 + (z1 - z0) * (j + 1) // k
+            out.append(HaloSlab((a, b), d, (max(0, a - d), min(n_z, b + d))))
+    return out
+
+
 def _split_gd_streamed(u: np.ndarray, slabs: list[HaloSlab],
                        params: TvParams) -> np.ndarray:
     """_split_gd with the windows kept in host memory and uploaded one at a
     time (out-of-core volumes).  ExactGlobal couples the windows every inner
-    iteration, so each iteration is two passes: the window sums of g^2
-    (cs_tv_grad_sumsq), then the step with the total (cs_tv_step, which
-    recomputes g -- bit-identical to the stored-g pair); LocalApprox runs a
-    window's whole epoch on the device."""
-    u = u.copy()
+    iteration: each iteration is one pass over the windows, each window
+    uploaded once from page-locked memory, its gradient recomputed and the
+    step taken in place with the global norm (cs_tv_grad_store,
+    cs_tv_step_g), the next iteration's sums formed from the stepped window
+    (cs_tv_grad_store again) and the window drained back -- double-buffered
+    on three streams (upload of window i + 1 and download of window i - 1
+    overlap the compute of window i) over windows cut to half the planned
+    size.  LocalApprox runs a window's whole epoch on the device."""
+    n_z = u.shape[0]
+    u = torch.from_numpy(u).clone().numpy()     # threaded copy
     total_voxels = u.size
     exact = params.norm_mode is NormMode.EXACT_GLOBAL
     dev = torch.device("cuda", torch.cuda.current_device())
     ss = torch.zeros(1, dtype=torch.float64, device=dev)
     for _ in range(params.outer_syncs):
-        local = [u[s.window[0]:s.window[1]].copy() for s in slabs]
         if exact and params.inner_iters > 0:
-            # One pass over the windows per iteration (plus one for the
-            # first sums): each window, held in page-locked memory, is
-            # uploaded once, its gradient recomputed and the step taken in
-            # place with the global norm (cs_tv_grad_store, cs_tv_step_g),
-            # the next iteration's sums formed from the stepped window
-            # (cs_tv_grad_store again, into the same g), and the window
-            # drained back: one upload instead of two per window and
-            # iteration, and the two window-sized device buffers the
-            # planner assumed (regularization.py:197-210).
-            n = len(slabs)
-            pin = [torch.from_numpy(w).pin_memory() for w in local]
-            cores = [(s.core_in_window.start, s.core_in_window.stop)
-                     for s in slabs]
-            sums = torch.zeros(n, dtype=torch.float64, device=dev)
-            for i in range(n):
-                K.tv_grad_sumsq(pin[i].to(dev, non_blocking=True), cores[i],
-                                sums[i:i + 1])
-            scratch = torch.zeros(1, dtype=torch.float64, device=dev)
-            for it in range(params.inner_iters):
-                tot = sums.sum().reshape(1)
-                last = it == params.inner_iters - 1
-                nxt = torch.zeros(n, dtype=torch.float64, device=dev)
-                for i in range(n):
-                    wd = pin[i].to(dev, non_blocking=True)
-                    g = torch.empty_like(wd)
-                    K.tv_grad_store(wd, g, cores[i], scratch)
-                    K.tv_step_g(wd, g, wd, params.step, tot, 1.0)
-                    if not last:
-                        K.tv_grad_store(wd, g, cores[i], nxt[i:i + 1])
-                    pin[i].copy_(wd, non_blocking=True)
-                    torch.cuda.current_stream(dev).synchronize()
-                sums = nxt
-            local = [t.numpy() for t in pin]
-        else:
-            for i, w in enumerate(local):
-                wd = _h2d(w)
-                spare = torch.empty_like(wd)
-                g = torch.empty_like(wd)
-                scale = float(np.sqrt(total_voxels / wd.numel()))
-                for _ in range(params.inner_iters):
-                    K.tv_grad_store(wd, g, (0, wd.shape[0]), ss)
-                    K.tv_step_g(wd, g, spare, params.step, ss, scale)
-                    wd, spare = spare, wd
-                local[i] = wd.cpu().numpy()
+            _gd_exact_streamed(u, slabs, params, dev)
+            continue
+        local = [u[s.window[0]:s.window[1]].copy() for s in slabs]
+        for i, w in enumerate(local):
+            wd = _h2d(w)
+            spare = torch.empty_like(wd)
+            g = torch.empty_like(wd)
+            scale = float(np.sqrt(total_voxels / wd.numel()))
+            for _ in range(params.inner_iters):
+                K.tv_grad_store(wd, g, (0, wd.shape[0]), ss)
+                K.tv_step_g(wd, g, spare, params.step, ss, scale)
+                wd, spare = spare, wd
+            local[i] = wd.cpu().numpy()
         for s, w in zip(slabs, local):
             u[s.core_range[0]:s.core_range[1]] = w[s.core_in_window]
+    del n_z
     return u
+
+
+def _gd_exact_streamed(u: np.ndarray, slabs: list[HaloSlab],
+                       params: TvParams, dev: torch.device) -> None:
+    """One ExactGlobal epoch of _split_gd_streamed, in place on ``u``."""
+    subs = _stream_windows(slabs, u.shape[0])
+    nbuf = 2 if subs is not None else 1
+    wins = subs if subs is not None else slabs
+    n = len(wins)
+    pins = []
+    for s in wins:
+        w0, w1 = s.window
+        p = torch.empty((w1 - w0,) + u.shape[1:], dtype=torch.float32,
+                        pin_memory=True)
+        p.copy_(torch.from_numpy(u[w0:w1]))
+        pins.append(p)
+    cores = [(s.core_in_window.start, s.core_in_window.stop) for s in wins]
+    wmax = max(p.shape[0] for p in pins)
+    bufs = [torch.empty((wmax,) + u.shape[1:], dtype=torch.float32,
+                        device=dev) for _ in range(nbuf)]
+    gbufs = [torch.empty_like(b) for b in bufs]
+    comp = torch.cuda.current_stream(dev)
+    up, down = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    slot_free = [None] * nbuf   # the slot's last user is done with it
+    drained = [None] * n        # window i's page-locked copy is current
+    k = [0]
+
+    def event(stream):
+        e = torch.cuda.Event()
+        e.record(stream)
+        return e
+
+    def stage(i):
+        slot = k[0] % nbuf
+        k[0] += 1
+        w = pins[i].shape[0]
+        dv, gv = bufs[slot][:w], gbufs[slot][:w]
+        for e in (slot_free[slot], drained[i]):
+            if e is not None:
+                up.wait_event(e)
+        with torch.cuda.stream(up):
+            dv.copy_(pins[i], non_blocking=True)
+        comp.wait_event(event(up))
+        return slot, dv, gv
+
+    def drain(i, slot, dv):
+        down.wait_event(event(comp))
+        with torch.cuda.stream(down):
+            pins[i].copy_(dv, non_blocking=True)
+        slot_free[slot] = drained[i] = event(down)
+
+    sums = torch.zeros(n, dtype=torch.float64, device=dev)
+    for i in range(n):
+        slot, dv, _ = stage(i)
+        K.tv_grad_sumsq(dv, cores[i], sums[i:i + 1])
+        slot_free[slot] = event(comp)
+    scratch = torch.zeros(1, dtype=torch.float64, device=dev)
+    for it in range(params.inner_iters):
+        tot = sums.sum().reshape(1)
+        last = it == params.inner_iters - 1
+        nxt = torch.zeros(n, dtype=torch.float64, device=dev)
+        for i in range(n):
+            slot, dv, gv = stage(i)
+            K.tv_grad_store(dv, gv, cores[i], scratch)
+            K.tv_step_g(dv, gv, dv, params.step, tot, 1.0)
+            if not last:
+                K.tv_grad_store(dv, gv, cores[i], nxt[i:i + 1])
+            drain(i, slot, dv)
+        sums = nxt
+    torch.cuda.synchronize(dev)
+    for s, p in zip(wins, pins):
+        z0, z1 = s.core_range
+        torch.from_numpy(u[z0:z1]).copy_(p[s.core_in_window])
 
 
 def _split_rof_streamed(f: np.ndarray, slabs: list[HaloSlab],
