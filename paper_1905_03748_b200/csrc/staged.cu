@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
           if (gy >= 0 && gy < ny && gz >= z_lo && gz < z_hi) {
             const float* src = vol_in + (size_t)(gz - z_lo) * plane +
                                (size_t)gy * nx;
-            if (vec_ok && gx >= 0 && gx + 3 < nx) {
+            if ((vec_ok & 1) && gx >= 0 && gx + 3 < nx) {
               q4 = __ldg(reinterpret_cast<const float4*>(src + gx));
             } else {
               if (gx >= 0 && gx < nx) q4.x = __ldg(src + gx);
@@ -676,7 +676,61 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
       else
         march(std::integral_constant<int, 0>());
     }
-    if (OP == OP_BWD && fits) {
+    if (OP == OP_BWD && !DET && M == 1 && fits && !prec && (vec_ok & 2)) {
+      // (A/B, CS_ST_BULK=1) flush through the TMA engine: the box's x-quads
+      // are converted to fp32 in place (int 0 and +0.f share their bits, so
+      // zero quads stay), then every in-grid (y, z) row of the box is added
+      // into the volume by one cp.reduce.async.bulk .add.f32 (UBLKRED) from
+      // shared memory -- no per-thread REDs through the LSU -- and the box
+      // is zeroed for the next chunk once the engine has read it
+      __syncthreads();
+      const int qpr_ = bn[0] >> 2;
+      const int nrow = bn[1] * bn[2];
+      const int nq = qpr_ * nrow;
+      const float rq = 1.f / (float)qpr_;
+      for (int qi = threadIdx.x; qi < nq; qi += ST_THREADS) {
+        const int row = small_div(qi, qpr_, rq);
+        int* bp = box_i + row * sy + 4 * (qi - row * qpr_);
+        const int4 q = *reinterpret_cast<const int4*>(bp);
+        if (q.x | q.y | q.z | q.w)
+          *reinterpret_cast<float4*>(bp) =
+              make_float4((float)q.x * inv_scale, (float)q.y * inv_scale,
+                          (float)q.z * inv_scale, (float)q.w * inv_scale);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      const int gx0 = max(bo[0], 0), gx1 = min(bo[0] + bn[0], nx);
+      bool issued = false;
+      if (gx1 > gx0) {
+        const float rb1 = 1.f / (float)bn[1];
+        const unsigned sbase = (unsigned)__cvta_generic_to_shared(
+            box_i + (gx0 - bo[0]));
+        const unsigned nbytes = (unsigned)(gx1 - gx0) * 4u;
+        for (int row = threadIdx.x; row < nrow; row += ST_THREADS) {
+          const int bz = small_div(row, bn[1], rb1);
+          const int gy = bo[1] + row - bz * bn[1], gz = bo[2] + bz;
+          if (gy < 0 || gy >= ny || gz < z_lo || gz >= z_hi) continue;
+          float* gp = vol_acc + (size_t)(gz - z_lo) * plane +
+                      (size_t)gy * nx + gx0;
+          asm volatile(
+              "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 "
+              "[%0], [%1], %2;" ::"l"(gp),
+              "r"(sbase + 4u * (unsigned)(row * sy)), "r"(nbytes)
+              : "memory");
+          issued = true;
+        }
+      }
+      if (issued) {
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+      __syncthreads();
+      for (int qi = threadIdx.x; qi < nq; qi += ST_THREADS) {
+        const int row = small_div(qi, qpr_, rq);
+        *reinterpret_cast<int4*>(box_i + row * sy + 4 * (qi - row * qpr_)) =
+            make_int4(0, 0, 0, 0);
+      }
+    } else if (OP == OP_BWD && fits) {
       __syncthreads();
       // flush the box: one 16-byte reduction per aligned x-quad.  A thread
       // owns one (x-quad, y) column of the box and walks it in z with
@@ -717,7 +771,7 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
         const int gx = bo[0] + 4 * xq, gy = bo[1] + by;
         const bool row_in = gy >= 0 && gy < ny;
         if (!CS_ST_ZOF && !row_in) continue;
-        const bool vec = vec_ok && gx >= 0 && gx + 3 < nx;
+        const bool vec = (vec_ok & 1) && gx >= 0 && gx + 3 < nx;
         const int* bp = box_i + (by * sy + 4 * xq * sx + bzs * sz) * wps;
         float* gp = vol_acc + (size_t)(bo[2] + bzs - z_lo) * plane +
                     (size_t)gy * nx + gx;
@@ -1046,7 +1100,12 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     edge = (int)fmin(ceil(1.0 / fmax(fp, 1e-3)) + 1.0, (double)max(n_u, n_v));
   }
   const void* vbase = OP == OP_BWD ? (const void*)vol_acc : (const void*)vol_in;
-  const int vec_ok = (nx % 4 == 0) && (((uintptr_t)vbase & 15) == 0);
+  // bit 0: 16-byte volume rows; bit 1: matched bulk-reduce flush (A/B knob
+  // CS_ST_BULK=1, y-major boxes, see the kernel)
+  static const char* bulk_knob = getenv("CS_ST_BULK");
+  const int bulk = OP == OP_BWD && bulk_knob && bulk_knob[0] == '1' ? 2 : 0;
+  const int vec_ok = (nx % 4 == 0) && (((uintptr_t)vbase & 15) == 0)
+                         ? 1 | bulk : 0;
   // v-band culling per main-axis class (runtime.cu slab_row_band); the
   // overwrite-mode Ax zeroes the culled rows
   int band[2][2] = {{0, n_v}, {0, n_v}};
@@ -1246,7 +1305,7 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     if (!rc && e2 == cudaSuccess)
       e2 = cudaMemsetAsync(acc_t, 0, slab_bytes, s);
     if (!rc && e2 == cudaSuccess) {
-      const int vec_t = (ny % 4 == 0);
+      const int vec_t = (ny % 4 == 0) ? 1 | bulk : 0;
       k1<<<grid_of(gx, rows(0), nviews(nxm)), ST_THREADS, smem, s>>>(
           vol_in, acc_t, dgeom_t, ids, GT, step_max, z_lo, z_hi, n_u, n_v,
           band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_t,
