@@ -994,6 +994,37 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Deterministic mode with the transposed frame: vol[z][y][x] += (acc[z][y][x]
+// + acc_t[z][x][y]) / S -- the two integer accumulators (same S) summed
+// exactly, then rounded once like det_finish_kernel (32 x 32 tiles of acc_t
+// through shared memory, coalesced on both sides).
+__global__ void __launch_bounds__(256)
+    det_finish_t_kernel(float* __restrict__ vol,
+                        const long long* __restrict__ acc,
+                        const long long* __restrict__ acc_t, int nx, int ny,
+                        const double* __restrict__ dscale) {
+  __shared__ long long tile[32][33];
+  const double S = *dscale;
+  const size_t plane = (size_t)nx * ny;
+  const long long* src = acc_t + (size_t)blockIdx.z * plane;
+  const int x0 = blockIdx.y * 32, y0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int x = x0 + i, y = y0 + threadIdx.x;
+    tile[i][threadIdx.x] = (x < nx && y < ny) ? src[(size_t)x * ny + y] : 0;
+  }
+  __syncthreads();
+  if (S == 0.0) return;
+  const double inv = 1.0 / S;   // a power of two: exact
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int y = y0 + i, x = x0 + threadIdx.x;
+    if (x < nx && y < ny) {
+      const size_t gi = (size_t)blockIdx.z * plane + (size_t)y * nx + x;
+      const long long q = acc[gi] + tile[threadIdx.x][i];
+      if (q) vol[gi] += (float)((double)q * inv);
+    }
+  }
+}
+
 static int g_deterministic = -1;   // -1: CS_ST_DETERMINISTIC decides
 
 static bool deterministic_matched() {
@@ -1046,12 +1077,13 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   bool use_t = false;
   const size_t slab_bytes = (size_t)(z_hi - z_lo) * nx * ny * sizeof(float);
   const bool det = OP == OP_BWD && deterministic_matched();
-  if (OP == OP_BWD && nxm > 0 && !det) {
+  if (OP == OP_BWD && nxm > 0) {
+    // deterministic mode: two int64 accumulators (direct + transposed)
     static const char* tk = getenv("CS_ST_TRANSPOSE");
     size_t free_b = 0, total_b = 0;
     use_t = !(tk && tk[0] == '0') &&
             cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
-            free_b > slab_bytes + ((size_t)4 << 30);
+            free_b > (det ? 4 : 1) * slab_bytes + ((size_t)4 << 30);
   }
   // Occupancy: with every matched view y-major (transposed frame) 4 CTAs x
   // 54 KB win (512^3: 250.6 vs 243.2 GUPS dense for 3 x 72 KB; 1024^3: 261.9
@@ -1244,9 +1276,11 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   // spreads a warp's REDs over 32 rows: 34.2 vs 24.3 ms per 45 views at
   // 512^3 (profiles/ncu_r02w.md).  Needs a slab-sized buffer: used when the
   // device has room for it (knob CS_ST_TRANSPOSE=0 disables).
-  // deterministic mode: a slab-sized int64 accumulator (x-major views in
-  // their own frame, so one accumulator serves both classes)
+  // deterministic mode: a slab-sized int64 accumulator, plus a transposed
+  // one for the x-major views when they run in the transposed frame (both
+  // in units of the same S, summed exactly by det_finish_t_kernel)
   long long* dacc = nullptr;
+  long long* dacc_t = nullptr;  // deterministic + transposed frame
   unsigned* dgmax = nullptr;   // [0]: max |proj| bits; [2..3]: S (double)
   double* dscale = nullptr;
   double det_c = 0.0;
@@ -1298,30 +1332,41 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     const Grid GT = make_grid(grid6_t, ny, nx, nz);
     AngleGeom* dgeom_t = nullptr;
     float* acc_t = nullptr;
+    const size_t acc_bytes = det ? 2 * slab_bytes : slab_bytes;
     rc = upload_geometry(geom_t, n_a, s, &dgeom_t);
     free(geom_t);
     cudaError_t e2 = rc ? cudaErrorUnknown
-                        : cudaMallocAsync((void**)&acc_t, slab_bytes, s);
+                        : cudaMallocAsync((void**)&acc_t, acc_bytes, s);
     if (!rc && e2 == cudaSuccess)
-      e2 = cudaMemsetAsync(acc_t, 0, slab_bytes, s);
+      e2 = cudaMemsetAsync(acc_t, 0, acc_bytes, s);
     if (!rc && e2 == cudaSuccess) {
       const int vec_t = (ny % 4 == 0) ? 1 | bulk : 0;
+      // deterministic: acc_t is the transposed int64 accumulator (passed as
+      // both the offset base and dacc; the kernel never stores floats there)
       k1<<<grid_of(gx, rows(0), nviews(nxm)), ST_THREADS, smem, s>>>(
           vol_in, acc_t, dgeom_t, ids, GT, step_max, z_lo, z_hi, n_u, n_v,
           band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_t,
-          lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad, nullptr,
-          nullptr, vpair, nxm);
+          lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad,
+          det ? reinterpret_cast<long long*>(acc_t) : nullptr,
+          det ? dscale : nullptr, vpair, nxm);
       CS_COUNT_LAUNCH();
-      const dim3 tg((ny + 31) / 32, (nx + 31) / 32, z_hi - z_lo);
-      transpose_add_kernel<<<tg, dim3(32, 8), 0, s>>>(vol_acc, acc_t, nx,
-                                                      ny);
-      CS_COUNT_LAUNCH();
+      if (det) {
+        dacc_t = reinterpret_cast<long long*>(acc_t);  // finished below
+      } else {
+        const dim3 tg((ny + 31) / 32, (nx + 31) / 32, z_hi - z_lo);
+        transpose_add_kernel<<<tg, dim3(32, 8), 0, s>>>(vol_acc, acc_t, nx,
+                                                        ny);
+        CS_COUNT_LAUNCH();
+      }
       const cudaError_t e3 = cudaGetLastError();
-      cudaFreeAsync(acc_t, s);
+      if (!det) cudaFreeAsync(acc_t, s);
       release_geometry(dgeom_t, s);
       if (e3 != cudaSuccess) {  // a launch failure is an error, not a
         cudaFreeAsync(ids, s);  // fallback
         release_geometry(dgeom, s);
+        if (dacc_t) cudaFreeAsync(dacc_t, s);
+        if (dacc) cudaFreeAsync(dacc, s);
+        if (dgmax) cudaFreeAsync(dgmax, s);
         CS_CHECK_CUDA(e3);
       }
       transposed = true;
@@ -1349,7 +1394,15 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
         vpair, nall - nxm);
     CS_COUNT_LAUNCH();
   }
-  if (det) {
+  if (det && dacc_t) {
+    const dim3 tg((ny + 31) / 32, (nx + 31) / 32, z_hi - z_lo);
+    det_finish_t_kernel<<<tg, dim3(32, 8), 0, s>>>(vol_acc, dacc, dacc_t, nx,
+                                                   ny, dscale);
+    CS_COUNT_LAUNCH();
+    cudaFreeAsync(dacc_t, s);
+    cudaFreeAsync(dacc, s);
+    cudaFreeAsync(dgmax, s);
+  } else if (det) {
     det_finish_kernel<<<num_sms() * 8, 256, 0, s>>>(
         vol_acc, dacc, (size_t)(z_hi - z_lo) * nx * ny, dscale);
     CS_COUNT_LAUNCH();

@@ -101,3 +101,41 @@ def test_matched_deterministic_global_fallback_subprocess():
                     generator=torch.Generator(device="cuda").manual_seed(2))
     ref = O.bwd_matched(y.cpu().numpy(), to_oracle(g))
     assert rel_l2(outs[0], ref) <= TOL_OP
+
+
+def test_matched_deterministic_transposed_frame_subprocess():
+    """Deterministic mode runs the x-major views in the transposed frame
+    into a second (transposed) int64 accumulator, finished together with
+    the direct one (det_finish_t_kernel).  Against the x-major views in
+    their own frame (CS_ST_TRANSPOSE=0): the same box sums in the same
+    units of S, so the same volume up to chunks whose box fits in one
+    frame's padded layout and not in the other's (global path)."""
+    code = (
+        "import torch,sys;sys.path.insert(0,'.');"
+        "import numpy as np;"
+        "from conftest import synth_geometry;"
+        "from paper_1905_03748_b200 import kernels as K;"
+        "g=synth_geometry(64,48);d=g.detector;"
+        "y=torch.randn((48,d.n_v,d.n_u),device='cuda',"
+        "generator=torch.Generator(device='cuda').manual_seed(4));"
+        "acc=torch.zeros((64,64,64),device='cuda');"
+        "K.bwd_matched(y,g,(0,48),(0,64),acc);"
+        "np.save(sys.argv[1],acc.cpu().numpy())")
+    outs = {}
+    with tempfile.TemporaryDirectory() as td:
+        for t in ("1", "0"):
+            env = dict(os.environ, CS_ST_DETERMINISTIC="1",
+                       CS_ST_TRANSPOSE=t,
+                       PYTHONPATH=os.path.join(ROOT, "tests"))
+            fn = os.path.join(td, f"t{t}.npy")
+            subprocess.run([sys.executable, "-c", code, fn], cwd=ROOT,
+                           env=env, check=True, timeout=300)
+            outs[t] = np.load(fn)
+    assert rel_l2(outs["1"], outs["0"]) <= 1e-7, rel_l2(outs["1"], outs["0"])
+    import torch
+    g = synth_geometry(64, 48)
+    d = g.detector
+    y = torch.randn((48, d.n_v, d.n_u), device="cuda",
+                    generator=torch.Generator(device="cuda").manual_seed(4))
+    ref = O.bwd_matched(y.cpu().numpy(), to_oracle(g))
+    assert rel_l2(outs["1"], ref) <= TOL_OP
