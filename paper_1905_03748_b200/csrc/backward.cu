@@ -240,11 +240,14 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
           const f32x2 fu2 = f2(fu, fu);
           auto tap = [&](int k) {
             const float vv = fmaf((float)k, dvz, vfrac);
-            const float fl = floorf(vv);
+            // floor by the 1.5 * 2^23 magic add rounded toward -inf (one
+            // FADD.RM on the FMA pipe instead of FRND on the conversion
+            // pipe): mb = 1.5 * 2^23 + floor(vv) exactly for |vv| < 2^22,
+            // its low mantissa bits the integer, mb - 1.5 * 2^23 == floorf
+            const float mb = __fadd_rd(vv, 12582912.f);
+            const float fl = mb - 12582912.f;
             const float fv = vv - fl;
-            // integral fl, |fl| < 2^22: int via the 1.5 * 2^23 magic add
-            const int il = __float_as_int(fl + 12582912.f) - 0x4B400000 +
-                           k * di;
+            const int il = __float_as_int(mb) - 0x4B400000 + k * di;
             const float* q = base + (row0 + il) * b.nu;
             const float t00 = q[0], t01 = q[1];
             const float t10 = q[b.nu], t11 = q[b.nu + 1];
