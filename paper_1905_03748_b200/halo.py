@@ -172,6 +172,27 @@ def split_minimize_distributed(u_full: torch.Tensor, slabs, params, rank: int,
         for _ in range(params.inner_iters):
             ops.rof_iter(f_loc, p, q, params.lam)
             p, q = q, p
+    # finish u = f + lam div p on this rank's core only: the ghost planes
+    # refreshed from the neighbours' cores supply p at z0 - 1 (div reads
+    # p at z - 1; the sub-slab's own first / last planes take the volume-
+    # face formula and are dropped unless they are the volume's faces),
+    # then one volume-sized gather of u instead of the 3-volume dual
+    exchange_halos(p, slabs, rank, zdim=1)
+    nz = f.shape[0]
+    z0, z1 = s.core_range
+    a, b = max(0, z0 - 1), min(nz, z1 + 1)
+    if a >= w0 and b <= w1:
+        ua = torch.empty((b - a,) + tuple(f.shape[1:]), dtype=f.dtype,
+                         device=f.device)
+        ops.rof_finish(f[a:b].contiguous(),
+                       p.narrow(1, a - w0, b - a).contiguous(), ua,
+                       params.lam)
+        u_w = torch.zeros((w1 - w0,) + tuple(f.shape[1:]), dtype=f.dtype,
+                          device=f.device)
+        u_w[z0 - w0:z1 - w0] = ua[z0 - a:z1 - a]
+        return gather_cores(u_w, slabs, rank, tuple(f.shape))
+    # zero-depth halos: no ghost plane in the window, finish on the
+    # gathered dual
     p_full = gather_cores(p, slabs, rank, None, zdim=1).contiguous()
     u = torch.empty_like(f)
     ops.rof_finish(f.contiguous(), p_full, u, params.lam)
