@@ -102,7 +102,9 @@ int cs_bwd_matched(float* vol_acc, int nx, int ny, int nz, int z_lo,
  * a voxel -- varies from run to run.  On: the contributions are rounded
  * once to a launch-wide fixed point and summed as 64-bit integers in a
  * slab-sized scratch accumulator (8 B per voxel, from CUDA's stream-ordered
- * pool), then added into vol_acc: bit-identical results every run, as the
+ * pool; a second, transposed one when the x-major views run in the
+ * transposed frame), then added into vol_acc: bit-identical results every
+ * run, as the
  * reference's fp64 host accumulation is (_kernels.py:278-337). */
 int cs_set_deterministic(int on);
 
