@@ -97,6 +97,13 @@ __global__ void __launch_bounds__(128)
 #ifndef CS_FS_CAP
 #define CS_FS_CAP 7168
 #endif
+// (A/B, -DCS_FS_PAIRS=1) footprint staged as column pairs, one LDS.64 per
+// bilinear row instead of two LDS: 826 vs 896 GUPS at config 2 (twice the
+// staging loads and 8-byte shared rows), not kept
+// (profiles/ab_fdk_pairs_r02ci.jsonl)
+#ifndef CS_FS_PAIRS
+#define CS_FS_PAIRS 0
+#endif
 constexpr int FS_TX = 16, FS_TY = 8, FS_NB = 16, FS_CAP = CS_FS_CAP;
 
 struct FsBox {
@@ -111,7 +118,13 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
                       double dsd, double inv_du, double inv_dv, double off_u,
                       double off_v, int n_u, int n_v,
                       float* __restrict__ vol) {
+#if CS_FS_PAIRS
+  // footprint as column pairs (t[v][u], t[v][u + 1]): one LDS.64 per
+  // bilinear row instead of two LDS
+  __shared__ float2 sbox2[FS_CAP / 2];
+#else
   __shared__ float sbox[FS_CAP];
+#endif
   __shared__ FsBox sb[FS_NB];
   __shared__ int s_m;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * FS_TX + tx;
@@ -179,7 +192,7 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
       int off = 0, m = 0;
       for (; m < FS_NB && a0 + m < n_a; m++) {
         const int sz = sb[m].nu * sb[m].nv;
-        if (off + sz > FS_CAP) break;
+        if (off + sz > (CS_FS_PAIRS ? FS_CAP / 2 : FS_CAP)) break;
         sb[m].off = off;
         off += sz;
       }
@@ -199,9 +212,17 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
         const int dr = NT / b.nu, dc = NT - dr * b.nu;
         for (int e = tid; e < b.nu * b.nv; e += NT) {
           const int u = b.u0 + c, v = b.v0 + r;
+#if CS_FS_PAIRS
+          const bool vin = v >= 0 && v < n_v;
+          const float* rowp = pj + (size_t)v * n_u;
+          sbox2[b.off + e] = make_float2(
+              (vin && u >= 0 && u < n_u) ? __ldg(rowp + u) : 0.f,
+              (vin && u + 1 >= 0 && u + 1 < n_u) ? __ldg(rowp + u + 1) : 0.f);
+#else
           sbox[b.off + e] = (u >= 0 && u < n_u && v >= 0 && v < n_v)
                                 ? __ldg(pj + (size_t)v * n_u + u)
                                 : 0.f;
+#endif
           c += dc;
           r += dr;
           if (c >= b.nu) {
@@ -236,7 +257,11 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
           const FsBox b = sb[j];
           const int col = (int)fu0 - b.u0;
           const int row0 = (int)fv0 - b.v0;
+#if CS_FS_PAIRS
+          const float2* base = sbox2 + b.off + col;
+#else
           const float* base = sbox + b.off + col;
+#endif
           const f32x2 fu2 = f2(fu, fu);
           auto tap = [&](int k) {
             const float vv = fmaf((float)k, dvz, vfrac);
@@ -248,9 +273,15 @@ __global__ void __launch_bounds__(FS_TX * FS_TY, FS_MINB)
             const float fl = mb - 12582912.f;
             const float fv = vv - fl;
             const int il = __float_as_int(mb) - 0x4B400000 + k * di;
+#if CS_FS_PAIRS
+            const float2* q = base + (row0 + il) * b.nu;
+            const float2 qa = q[0], qb = q[b.nu];
+            const float t00 = qa.x, t01 = qa.y, t10 = qb.x, t11 = qb.y;
+#else
             const float* q = base + (row0 + il) * b.nu;
             const float t00 = q[0], t01 = q[1];
             const float t10 = q[b.nu], t11 = q[b.nu + 1];
+#endif
             // both row lerps in one FADD2 + FFMA2 (bit-identical to the
             // scalar fmaf(fu, t01 - t00, t00), fmaf(fu, t11 - t10, t10))
             const f32x2 lo = f2(t00, t10);
