@@ -574,18 +574,23 @@ def run_c3_steps(args, g, ops, x, dev, local, backend, steps=None,
                "bwd_matched_kernel" if t_atb >= t_ax else "fwd_mlayer_kernel",
                max(t_atb, t_ax), upd_half / ops.world,
                bytes_per_update(n, n)),
-           "e2e": c3_e2e(ops, x, b_meas, w, blocks, dev, backend)}
+           "e2e": c3_e2e(ops, x, b_meas, w, blocks, dev, backend,
+                         upd=upd, res=res)}
     out["roofline"]["note"] = ("per-rank half-step (rank 0's share of the "
                                "block, incl. its collectives) as one launch")
     del K
     return out
 
 
-def c3_e2e(ops, x, b_dev, w, blocks, dev, backend, reps=2):
+def c3_e2e(ops, x, b_dev, w, blocks, dev, backend, reps=2, upd=None,
+           res=None):
     """End to end per step through the public sharded API: the block's
     measured projections (this rank's shard) copied in from pinned host
     memory, the step, and the block's residual norm read back (the loop
-    metric); slowest rank."""
+    metric); slowest rank.  Reuses the device step's update and residual
+    buffers: a second slab-sized update would take the memory the matched
+    kernel's transposed frame needs (at N = 1 a 32 GiB volume) and time a
+    different kernel path than the device step."""
     import torch
     import torch.distributed as dist
     from paper_1905_03748_b200.sharded import CudaVecOps
@@ -593,8 +598,8 @@ def c3_e2e(ops, x, b_dev, w, blocks, dev, backend, reps=2):
     host = torch.empty(b_dev.shape, dtype=torch.float32, pin_memory=True)
     host.copy_(b_dev)
     b = torch.empty_like(b_dev)
-    res = torch.empty_like(b_dev)
-    upd = torch.zeros_like(x)
+    res = torch.empty_like(b_dev) if res is None else res
+    upd = torch.zeros_like(x) if upd is None else upd
     blk = blocks[0]
     s0, s1 = ops.shard(blk)
 

@@ -1075,15 +1075,37 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
   // when the device has room for a slab-sized accumulator (see the launch
   // below; knob CS_ST_TRANSPOSE=0 disables).
   bool use_t = false;
-  const size_t slab_bytes = (size_t)(z_hi - z_lo) * nx * ny * sizeof(float);
+  const size_t plane_bytes = (size_t)nx * ny * sizeof(float);
+  const size_t slab_bytes = (size_t)(z_hi - z_lo) * plane_bytes;
   const bool det = OP == OP_BWD && deterministic_matched();
+  int t_planes = z_hi - z_lo;  // planes per transposed-frame piece
   if (OP == OP_BWD && nxm > 0) {
     // deterministic mode: two int64 accumulators (direct + transposed)
     static const char* tk = getenv("CS_ST_TRANSPOSE");
     size_t free_b = 0, total_b = 0;
-    use_t = !(tk && tk[0] == '0') &&
-            cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
-            free_b > (det ? 4 : 1) * slab_bytes + ((size_t)4 << 30);
+    const size_t margin = (size_t)4 << 30;
+    if (!(tk && tk[0] == '0') &&
+        cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+      if (free_b > (det ? 4 : 1) * slab_bytes + margin) {
+        use_t = true;
+      } else if (!det && free_b > margin) {
+        // no room for a slab-sized accumulator (e.g. a 2048^3 slab beside
+        // its cached Ax textures): the x-major views in z pieces of the
+        // slab, each into a piece-sized accumulator; pieces of at least
+        // 64 planes and 1/8 of the slab (thinner ones re-walk too many
+        // rays per plane)
+        const size_t fit = (free_b - margin) / plane_bytes;
+        const size_t need = (size_t)max(64, (z_hi - z_lo + 7) / 8);
+        if (fit >= need) {
+          use_t = true;
+          t_planes = (int)fit;
+        }
+      }
+      // (test knob) CS_ST_TPIECE=n: z pieces of n planes
+      static const char* tp_piece = getenv("CS_ST_TPIECE");
+      if (use_t && !det && tp_piece && atoi(tp_piece) > 0)
+        t_planes = atoi(tp_piece);
+    }
   }
   // Occupancy: with every matched view y-major (transposed frame) 4 CTAs x
   // 54 KB win (512^3: 250.6 vs 243.2 GUPS dense for 3 x 72 KB; 1024^3: 261.9
@@ -1332,7 +1354,9 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
     const Grid GT = make_grid(grid6_t, ny, nx, nz);
     AngleGeom* dgeom_t = nullptr;
     float* acc_t = nullptr;
-    const size_t acc_bytes = det ? 2 * slab_bytes : slab_bytes;
+    const size_t acc_bytes =
+        det ? 2 * slab_bytes
+            : (size_t)min(t_planes, z_hi - z_lo) * plane_bytes;
     rc = upload_geometry(geom_t, n_a, s, &dgeom_t);
     free(geom_t);
     cudaError_t e2 = rc ? cudaErrorUnknown
@@ -1343,22 +1367,30 @@ int launch_staged(const float* vol_in, float* vol_acc, int nx, int ny, int nz,
       const int vec_t = (ny % 4 == 0) ? 1 | bulk : 0;
       // deterministic: acc_t is the transposed int64 accumulator (passed as
       // both the offset base and dacc; the kernel never stores floats there)
-      k1<<<grid_of(gx, rows(0), nviews(nxm)), ST_THREADS, smem, s>>>(
-          vol_in, acc_t, dgeom_t, ids, GT, step_max, z_lo, z_hi, n_u, n_v,
-          band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_t,
-          lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad,
-          det ? reinterpret_cast<long long*>(acc_t) : nullptr,
-          det ? dscale : nullptr, vpair, nxm);
-      CS_COUNT_LAUNCH();
-      if (det) {
-        dacc_t = reinterpret_cast<long long*>(acc_t);  // finished below
-      } else {
-        const dim3 tg((ny + 31) / 32, (nx + 31) / 32, z_hi - z_lo);
-        transpose_add_kernel<<<tg, dim3(32, 8), 0, s>>>(vol_acc, acc_t, nx,
-                                                        ny);
+      // and covers the whole slab; otherwise z pieces of t_planes planes,
+      // each accumulated and transposed-added before the next reuses acc_t
+      for (int zl = z_lo; zl < z_hi; zl += t_planes) {
+        const int zh = min(z_hi, zl + t_planes);
+        if (!det && zl > z_lo) {
+          e2 = cudaMemsetAsync(acc_t, 0, (size_t)(zh - zl) * plane_bytes, s);
+          if (e2 != cudaSuccess) break;
+        }
+        k1<<<grid_of(gx, rows(0), nviews(nxm)), ST_THREADS, smem, s>>>(
+            vol_in, acc_t, dgeom_t, ids, GT, step_max, zl, zh, n_u, n_v,
+            band[0][0], band[0][1], out, proj_in, rb, rw, cap, budget, vec_t,
+            lane_stride, prec_mode, prec_fp, edge, lo_scale, tpad,
+            det ? reinterpret_cast<long long*>(acc_t) : nullptr,
+            det ? dscale : nullptr, vpair, nxm);
         CS_COUNT_LAUNCH();
+        if (!det) {
+          const dim3 tg((ny + 31) / 32, (nx + 31) / 32, zh - zl);
+          transpose_add_kernel<<<tg, dim3(32, 8), 0, s>>>(
+              vol_acc + (size_t)(zl - z_lo) * nx * ny, acc_t, nx, ny);
+          CS_COUNT_LAUNCH();
+        }
       }
-      const cudaError_t e3 = cudaGetLastError();
+      if (det) dacc_t = reinterpret_cast<long long*>(acc_t);  // finished below
+      const cudaError_t e3 = e2 != cudaSuccess ? e2 : cudaGetLastError();
       if (!det) cudaFreeAsync(acc_t, s);
       release_geometry(dgeom_t, s);
       if (e3 != cudaSuccess) {  // a launch failure is an error, not a

@@ -926,7 +926,8 @@ def test_matched_transposed_frame_subprocess():
     """Matched Atb's x-major views run as y-major views of the transposed
     frame (staged.cu); the direct x-major launch (CS_ST_TRANSPOSE=0) gives
     the same box sums, so the two agree to fp32 summation order -- on odd,
-    non-multiple-of-4 sizes with anisotropic voxels, offsets and a slab."""
+    non-multiple-of-4 sizes with anisotropic voxels, offsets and a slab;
+    likewise the transposed frame in z pieces (CS_ST_TPIECE)."""
     import os
     import subprocess
     import sys
@@ -950,15 +951,21 @@ def test_matched_transposed_frame_subprocess():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     with tempfile.TemporaryDirectory() as td:
         outs = []
-        for tag, env_add in (("t", {}), ("direct", {"CS_ST_TRANSPOSE": "0"})):
+        for tag, env_add in (("t", {}), ("direct", {"CS_ST_TRANSPOSE": "0"}),
+                             ("pieces", {"CS_ST_TPIECE": "4"})):
             fn = os.path.join(td, f"{tag}.pt")
             subprocess.run([sys.executable, "-c", code, fn], cwd=root,
                            env=dict(os.environ, **env_add), check=True)
             outs.append(torch_load(fn))
-    (a1, a2), (b1, b2) = outs
+    (a1, a2), (b1, b2), (c1, c2) = outs
     assert rel_l2(a1.numpy(), b1.numpy()) <= 1e-6
     assert rel_l2(a2.numpy(), b2.numpy()) <= 1e-6
     assert rel_l2(a2.numpy(), b1.numpy()[7:16]) <= 1e-6
+    # the transposed frame in z pieces of 4 planes (the path taken when a
+    # slab-sized accumulator does not fit): pieces of 23 and of the 9-plane
+    # slab, each accumulated and transposed-added in turn
+    assert rel_l2(c1.numpy(), b1.numpy()) <= 1e-6
+    assert rel_l2(c2.numpy(), b2.numpy()) <= 1e-6
 
 
 def torch_load(path):
