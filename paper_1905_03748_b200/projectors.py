@@ -159,6 +159,65 @@ def _chunked_from_host(data: np.ndarray, device, launch, a0: int, a1: int):
     side.synchronize()  # the host source may be released after return
 
 
+# host-to-host backprojection: the last view chunk runs in this many z
+# pieces, each drained to the host while the next one computes, when the
+# slab is at least _DRAIN_PIECE_MIN_BYTES (the volume's device->host copy,
+# ~10 ms per 512^3, otherwise follows the whole computation)
+_DRAIN_PIECES = 4
+_DRAIN_PIECE_MIN_BYTES = 64 << 20
+
+
+def _backproject_to_host(data: np.ndarray, geometry, slab_range, bwd,
+                         a0: int, a1: int, device) -> np.ndarray:
+    """backproject_slab for host projections into a fresh host volume:
+    view chunks uploaded on a side stream while the previous chunk
+    backprojects (as _chunked_from_host); the last chunk's backprojection
+    is cut into z pieces (Atb is additive over views and separable over
+    slabs), and each finished piece of the volume drains to one pinned host
+    array on the side stream while the next piece computes."""
+    z0, z1 = slab_range
+    grid = geometry.voxel_grid
+    cur = torch.cuda.current_stream(device)
+    side = _side_stream(device)
+    target = torch.zeros((z1 - z0, grid.n_y, grid.n_x), dtype=torch.float32,
+                         device=device)
+    host = torch.empty(tuple(target.shape), dtype=torch.float32,
+                       pin_memory=target.numel() * 4 >= _PINNED_MIN_BYTES)
+    src = torch.from_numpy(np.ascontiguousarray(data, dtype=DTYPE))
+    dev = torch.empty(tuple(src.shape), dtype=torch.float32, device=device)
+    side.wait_stream(cur)  # dev / target memory may be reused from cur's work
+    n_p = (_DRAIN_PIECES if target.numel() * 4 >= _DRAIN_PIECE_MIN_BYTES
+           else 1)
+    n_p = max(1, min(n_p, z1 - z0))
+    starts = list(range(a0, a1, _DRAIN_VIEWS))
+    for c0 in starts:
+        c1 = min(a1, c0 + _DRAIN_VIEWS)
+        with torch.cuda.stream(side):
+            dev[c0 - a0:c1 - a0].copy_(src[c0 - a0:c1 - a0],
+                                       non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(side)
+        cur.wait_event(ev)
+        chunk = dev[c0 - a0:c1 - a0]
+        if c0 != starts[-1]:
+            bwd(chunk, geometry, (c0, c1), (z0, z1), target)
+            continue
+        for i in range(n_p):
+            p0 = z0 + (z1 - z0) * i // n_p
+            p1 = z0 + (z1 - z0) * (i + 1) // n_p
+            piece = target[p0 - z0:p1 - z0]
+            bwd(chunk, geometry, (c0, c1), (p0, p1), piece)
+            done = torch.cuda.Event()
+            done.record(cur)
+            side.wait_event(done)
+            with torch.cuda.stream(side):
+                host[p0 - z0:p1 - z0].copy_(piece, non_blocking=True)
+    dev.record_stream(cur)
+    target.record_stream(side)
+    side.synchronize()  # the host source may be released after return
+    return host.numpy()
+
+
 _SIDE = {}
 
 
@@ -407,6 +466,13 @@ def backproject_slab(projections: ProjectionStack, geometry: ScanGeometry,
     a0, a1 = projections.angle_range
     if not (0 <= a0 < a1 <= geometry.n_angles):
         raise ValueError(f"angle range {projections.angle_range} outside scan")
+    if accumulate_into is None and not projections.on_device:
+        if not isinstance(mode, WeightMode):
+            raise ValueError(f"unknown weight mode {mode}")
+        bwd = K.bwd_fdk if mode is WeightMode.FDK else K.bwd_matched
+        return Volume(grid, _backproject_to_host(
+            projections.data, geometry, (z0, z1), bwd, a0, a1, _device()),
+            (z0, z1))
     if accumulate_into is None:
         # fresh accumulator: zeros on the device; host callers get host data
         target = torch.zeros((z1 - z0, grid.n_y, grid.n_x),
