@@ -294,6 +294,9 @@ constexpr int TM_OX = 30, TM_OY = TM_WARPS - 2;
 #define CS_TM_ZC 32
 #endif
 constexpr int TM_ZC = CS_TM_ZC;
+#ifndef CS_TM_UNROLL2
+#define CS_TM_UNROLL2 1
+#endif
 constexpr int TM_NS = 8;         // ring stages (power of two)
 constexpr int TM_D = TM_NS;  // planes in flight (the ring slot reused is
                                // the one taken an iteration earlier)
@@ -700,6 +703,9 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
   const float mxb = (in_xy && x + 1 < W.nx - 1) ? 1.f : 0.f;
   const float my = (in_xy && y < W.ny - 1) ? 1.f : 0.f;
   const int zlo_sum = max(zb, c_lo), zhi_sum = own ? c_hi : INT_MIN;
+#if CS_TM_UNROLL2
+#pragma unroll 2
+#endif
   for (int z = zb - 1; z < ze; z++) {
     // the stage of plane z was read by every thread before the previous
     // plane's barrier: refill it (plane z + NS)
