@@ -54,6 +54,12 @@ constexpr int ST_THREADS = ST_TU * ST_TV;
 #ifndef CS_ST_VIEWFAST
 #define CS_ST_VIEWFAST 1
 #endif
+// (A/B, -DCS_ST_UNROLL2=1) the sample loop unrolled by two: dense 512^3
+// 255.8 vs 257.5 GUPS, 1024^3 267.7 vs 269.3 -- the kernel is bound by the
+// shared-atomic wavefronts, not issue (profiles/ab_matched_unroll2_r02cr.jsonl)
+#ifndef CS_ST_UNROLL2
+#define CS_ST_UNROLL2 0
+#endif
 #ifndef CS_ST_ZOF
 #define CS_ST_ZOF 1
 #endif
@@ -565,6 +571,9 @@ __global__ void __launch_bounds__(ST_THREADS, MINB)
         atomicAdd(box_i + b_cur + sz + sy, a6);
         atomicAdd(box_i + b_cur + sz + sy + sx, a7);
       };
+#endif
+#if CS_ST_UNROLL2
+#pragma unroll 2
 #endif
       for (int kk = ka; kk < kb;
            kk++, qx += m.Bq[0], qy += m.Bq[1], qz += m.Bq[2]) {
